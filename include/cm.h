@@ -1,0 +1,233 @@
+/*
+ * cm.h -- C ABI of libcm.so: the B200-native hot path of Checkmate (arXiv 2507.13522).
+ *
+ * The path: a per-iteration bucketed gradient all-reduce across the GPUs
+ * of one NVSwitch box whose reduced result is also "multicast" -- tapped exactly once
+ * into a pinned, host-mapped shadow ring -- plus the deterministic AdamW step that the
+ * training replica applies and that a shadow replica re-applies off the critical path,
+ * plus a restore path that rebuilds training state from the shadow.
+ *
+ *   PAPER.md:32 (sec 1)  "model updates are deterministic: given a model state at time t
+ *                         and its corresponding gradients, applying the optimizer step
+ *                         produces the state at time t+1"
+ *   PAPER.md:35          "replicates reduced gradients ... multicasts them to shadow nodes,
+ *                         which apply these updates to independently maintained replicas"
+ *
+ * Conventions for every call:
+ *   - Plain C types only.  `stream` arguments are cudaStream_t handles passed as void*
+ *     (NULL = the legacy default stream).  Device pointers are CUDA device addresses on
+ *     the context's device; host pointers are ordinary process addresses.
+ *   - No exception crosses the ABI.  Every call returns a cm_status; on failure a
+ *     message is available from cm_last_error(ctx).  CM_ERR_CUDA is sticky: once a CUDA
+ *     call failed the context refuses further work.
+ *   - Enqueueing calls (allreduce, apply, shadow apply, gen, restore) are asynchronous
+ *     with respect to the host: they enqueue kernels on `stream` and return.  Device-side
+ *     faults surface at the next call that synchronises.
+ *   - Thread safety: one context is driven by one host thread at a time.
+ *   - The library never falls back to a CPU implementation: without a usable CUDA
+ *     device cm_init fails with CM_ERR_CUDA.
+ */
+#ifndef CM_H_
+#define CM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cm_ctx cm_ctx; /* opaque; one per GPU rank (or per virtual rank) */
+
+/* Status codes.  0/2/3/4 follow SPEC.md:616 (ok / config / invariant / unrecoverable). */
+typedef enum {
+    CM_OK = 0,
+    CM_ERR_ARG = 1,           /* null / misaligned pointer, index out of range             */
+    CM_ERR_CONFIG = 2,        /* bad world size, ring depth, layer table, no peer access   */
+    CM_ERR_INVARIANT = 3,     /* verification mismatch (shadow != train), non-finite state */
+    CM_ERR_UNRECOVERABLE = 4, /* no consistent shadow step to restore from                 */
+    CM_ERR_CUDA = 5,          /* a CUDA call failed (sticky)                               */
+    CM_ERR_STATE = 6          /* call out of order: iteration gap, partial iteration,
+                                 layout mismatch, ring slot not released                   */
+} cm_status;
+
+typedef enum { CM_F32 = 0, CM_BF16 = 1 } cm_dtype; /* gradient dtype; state is always fp32 */
+
+/* Where the shadow replica's (p, m, v) lives.  The tap ring is host memory in both cases
+ * (north_star: "streams each reduced shard once into a pinned, host-mapped shadow ring").
+ *   HOST:   POSIX shared memory, survives the training process and the GPU (the analog of
+ *           the paper's separate CPU shadow cluster).
+ *   DEVICE: a library-owned HBM allocation outside the training buffers; survives only an
+ *           in-process ("soft") failure.  Arithmetic is identical in both placements.   */
+typedef enum { CM_SHADOW_HOST = 0, CM_SHADOW_DEVICE = 1 } cm_shadow_place;
+
+/* cm_config.flags */
+#define CM_FLAG_NO_TAP (1ull << 0)    /* all-reduce + AdamW only: no tap, no shadow (the
+                                         "no checkpoint" arm run on our own kernels)       */
+#define CM_FLAG_ATTACH (1ull << 1)    /* attach to an existing shadow segment (restart
+                                         after a failure) instead of creating a fresh one  */
+#define CM_FLAG_TAP_COPYENGINE (1ull << 2) /* ablation: tap with a copy-engine D2H after
+                                         the all-reduce kernel instead of in-kernel stores */
+
+typedef struct {
+    int32_t world_size;   /* n, 1..8: data-parallel ranks on this box                      */
+    int32_t rank;         /* r, 0..n-1                                                      */
+    int32_t device;       /* CUDA device ordinal this rank uses                             */
+    int32_t ring_depth;   /* D >= 2: iterations the tap ring holds (flow-control window)    */
+    int32_t shadow_place; /* cm_shadow_place                                                */
+    int32_t reserved;
+    const char *shm_name; /* base name of the shadow segment; rank r uses "/<name>.r<r>".
+                             Required unless CM_FLAG_NO_TAP.  Copied by cm_init.            */
+    uint64_t flags;       /* CM_FLAG_*                                                      */
+} cm_config;
+
+/* The model's parameter tensors in model order ("bin-packing them, starting
+ * from the last model layer and working backwards").  numel[i] > 0.       */
+typedef struct {
+    const int64_t *numel;
+    int32_t n_tensors;
+    int32_t grad_dtype; /* cm_dtype */
+    int64_t cap_bytes;  /* bucket cap in bytes of the gradient dtype; 25 MiB in DDP     */
+} cm_layer_table;
+
+/* AdamW hyper-parameters for one step (defaults).  The
+ * caller's learning-rate schedule passes lr for the step (PAPER.md:496 uses cosine
+ * annealing); the library records it so the shadow applies identical bits (reading R8). */
+typedef struct {
+    double lr, beta1, beta2, eps, weight_decay;
+} cm_adamw;
+
+/* ------------------------------------------------------------------ planning (pure)
+ * cm_plan_buckets -- the bucket plan, PAPER.md:258-264 (sec 4.2.2), reading R10-R13:
+ * walk tensors from the last to the first; add a tensor to the open bucket while the
+ * bucket's bytes stay <= cap_bytes; a tensor larger than cap gets a dedicated bucket
+ * (closing the open one).  Each bucket is zero-padded to a multiple of n*V elements,
+ * V = 16 B / sizeof(grad), so it splits into n equal 16-byte-aligned shards.
+ * The flat layout is bucket 0 first; inside a bucket the tensors in the order added.
+ *   out_padded_numel   total flat elements P_pad (size every flat buffer to this)
+ *   out_n_buckets      number of buckets
+ *   tensor_elem_offset optional [n_tensors]: flat element offset of each tensor
+ * Host-only, no device needed.  CM_ERR_CONFIG on an empty/invalid table.            */
+cm_status cm_plan_buckets(const cm_layer_table *table, int32_t world_size,
+                          int64_t *out_padded_numel, int32_t *out_n_buckets,
+                          int64_t *tensor_elem_offset);
+
+/* ------------------------------------------------------------------ lifecycle
+ * cm_init -- create a context for one rank: select the device, allocate the signal pad
+ * used by the cross-GPU barriers.  CM_ERR_CONFIG for n outside 1..8, rank outside
+ * [0,n), D < 2; CM_ERR_CUDA if the device cannot be used.                             */
+cm_status cm_init(const cm_config *cfg, cm_ctx **out);
+
+/* cm_register_buckets -- plan the buckets and register the caller's flat buffers.
+ *   grad   device, P_pad elements of grad_dtype: this rank's gradients in the flat
+ *          layout; after cm_allreduce_multicast of bucket b it holds the reduced SUM.
+ *   p,m,v  device, P_pad fp32 each: master weights and AdamW moments (flat layout).
+ * All four must be 16-byte aligned, must outlive the context, and are owned by the
+ * caller.  Writes an opaque exchange blob (this rank's IPC handles) into blob_out; on
+ * entry *blob_len is its capacity (cm_blob_size() bytes suffice), on exit its length.
+ * CM_ERR_ARG for null/misaligned pointers; CM_ERR_CONFIG for a bad table.             */
+cm_status cm_register_buckets(cm_ctx *ctx, const cm_layer_table *table, void *grad,
+                              float *p, float *m, float *v, void *blob_out, size_t *blob_len);
+size_t cm_blob_size(void);
+
+/* cm_connect -- collective over the n ranks (each calls it with everyone's blobs, in
+ * rank order, concatenated: n * blob_len bytes, e.g. from torch all_gather_object).
+ * Maps the peers' buffers and signal pads (CUDA IPC over NVLink; in-process peers --
+ * "virtual ranks" on one GPU -- are used directly and need no barriers), creates (or
+ * with CM_FLAG_ATTACH attaches) the shadow segment, and -- when creating -- copies the
+ * step-0 state shard r into the shadow (reading R19, "a prior checkpoint
+ * replica").  Blocks until that copy is done.  CM_ERR_CONFIG if the blobs disagree on
+ * n / layout or a peer is not reachable; CM_ERR_STATE if an attached segment's layout
+ * differs.                                                              */
+cm_status cm_connect(cm_ctx *ctx, const void *peer_blobs, size_t blob_len);
+
+/* cm_finalize -- synchronise, unmap peers and the segment, free library memory.  The
+ * shadow segment is NOT unlinked (it is the restore source); see cm_unlink_shadow.     */
+cm_status cm_finalize(cm_ctx *ctx);
+cm_status cm_unlink_shadow(const char *shm_name, int32_t rank);
+const char *cm_last_error(const cm_ctx *ctx);
+
+/* ------------------------------------------------------------------ hot path
+ * cm_allreduce_multicast -- reduce-scatter + tap + all-gather of bucket b for iteration
+ * t, one fused sm_100a kernel on `stream` (sec 2.1 AllReduce =
+ * ReduceScatter + AllGather; sec 4.1.1 "deliver each reduced
+ * gradient to the shadow cluster exactly once per iteration").  Rank r owns shard r:
+ *   R[i] = (((g_0[i] + g_1[i]) + g_2[i]) + ... + g_{n-1}[i])   fp32, rank order (R2, R3)
+ * (bf16 grads: exact upcast, fp32 sum, one round-to-nearest-even to bf16, R14/R25), read
+ * from the n ranks' buffers over NVLink; stored once into the host ring slot t mod D
+ * (the tap) and into shard r of all n ranks' grad buffers (the all-gather).  In place:
+ * only rank r touches shard r of any buffer.  Cross-rank readiness is handled inside the
+ * kernel by epoch-tagged flags; the call is stream-ordered after the caller's writes of
+ * bucket b.  Before the first bucket of iteration t >= D, the stream waits until the
+ * shadow released slot t mod D (lossless backpressure, sec 4.3.3): if
+ * the matching cm_shadow_apply was never enqueued the call fails with CM_ERR_STATE
+ * instead of overwriting an unconsumed slot.  Iterations are consecutive (CM_ERR_STATE
+ * on a gap); buckets of one iteration may be issued in any order, each exactly once.  */
+cm_status cm_allreduce_multicast(cm_ctx *ctx, int32_t bucket, int64_t iteration, void *stream);
+
+/* cm_apply_step -- the training replica's AdamW step `step` = t+1 over all P_pad
+ * elements, one fused HBM-bound sm_100a kernel (reading R4):
+ *   g = R*inv_n; m = B1*m + c1*g; v = B2*v + c2*(g*g); mh = m/bc1; vh = v/bc2;
+ *   d = sqrt(vh) + eps; p = p - lr*(mh/d + wd*p)
+ * every op an IEEE fp32 op rounded to nearest, no FMA; scalars c1=1-b1, c2=1-b2,
+ * bc1=1-b1^s, bc2=1-b2^s, inv_n=1/n computed in fp64 on the host and rounded once (R5,
+ * R6).  Requires every bucket of iteration t to have been all-reduced (CM_ERR_STATE
+ * otherwise: "no partial update").  Records the step's scalars for the
+ * shadow.  With CM_FLAG_NO_TAP the all-reduce has no tap and no shadow exists.        */
+cm_status cm_apply_step(cm_ctx *ctx, int64_t step, const cm_adamw *hp, void *stream);
+
+/* cm_shadow_apply -- the shadow replica's step `step` (Listing 2, PAPER.md:290-298:
+ * "buckets.recv(); optimizer.step()"), enqueued on `side_stream`, off the training
+ * stream's critical path.  Waits (stream-ordered) until every tap of iteration step-1 is
+ * in the ring ("Once all gradients for an iteration are received"), then
+ * applies the identical AdamW to shard r of the shadow state, reading the ring slot and
+ * ping-pong half (step-1)&1, writing half step&1, publishes the step in the segment
+ * header and releases the ring slot.  step must be last+1 (CM_ERR_STATE: an iteration
+ * gap is fatal) and cm_apply_step(step) must have been called.          */
+cm_status cm_shadow_apply(cm_ctx *ctx, int64_t step, void *side_stream);
+
+/* cm_restore -- the failure path (PAPER.md:313-314 consolidation; sec 6.5 methodology,
+ * PAPER.md:601).  Collective over the n ranks.  Reads every rank's segment header,
+ * computes the consolidation step I (reading R21: the largest step every shard can reach
+ * -- its published step, its retained previous half, or by rolling forward over fully
+ * tapped ring slots), rolls this rank's shard forward to I if needed, copies it host ->
+ * device and all-gathers p/m/v to every rank over NVLink.  Blocks until done; returns I
+ * in *restored_step; the caller resumes at iteration I.  CM_ERR_UNRECOVERABLE if no
+ * common step exists.                                                                  */
+cm_status cm_restore(cm_ctx *ctx, int64_t *restored_step, void *stream);
+
+/* ------------------------------------------------------------------ inputs / checks
+ * cm_gen_grads -- synthetic gradients (gradient production) for this
+ * rank at iteration t into the registered grad buffer, from the counter-based generator
+ * of DESIGN.md "Input recipe" (SplitMix64; padding elements are zero).                 */
+cm_status cm_gen_grads(cm_ctx *ctx, uint64_t seed, int64_t iteration, int32_t scale, void *stream);
+/* cm_init_state -- p = p_0 from the generator (identical on every rank), m = v = 0.    */
+cm_status cm_init_state(cm_ctx *ctx, uint64_t seed, void *stream);
+
+/* cm_verify -- bitwise compare this rank's shadow shard (current half) with shard r of
+ * the training p, m, v.  Synchronises `stream`.  *mismatch = -1 if
+ * equal, else the flat index of the first differing element; CM_ERR_INVARIANT then.   */
+cm_status cm_verify(cm_ctx *ctx, int64_t *mismatch, void *stream);
+
+/* Introspection (host-only, cheap). */
+typedef struct {
+    int32_t n_buckets, world_size, rank, ring_depth, grad_dtype, shadow_place, peers_in_process;
+    int32_t reserved;
+    int64_t padded_numel, shard_numel;  /* P_pad; sum over buckets of E_b/n               */
+    int64_t shadow_step;                /* last step the shadow published                 */
+    int64_t launches;                   /* kernels this context launched so far           */
+    uint64_t layout_hash;
+} cm_info;
+cm_status cm_get_info(const cm_ctx *ctx, cm_info *out);
+cm_status cm_bucket_info(const cm_ctx *ctx, int32_t bucket, int64_t *elem_off, int64_t *padded,
+                         int64_t *used);
+/* Host pointers into the shadow: state half h (0/1) as shard-local arrays of
+ * shard_numel fp32 (HOST placement only; DEVICE placement returns device pointers),
+ * and ring slot k (shard-local, grad dtype).  For tests and tools.                     */
+cm_status cm_shadow_view(const cm_ctx *ctx, int32_t half, float **p, float **m, float **v);
+cm_status cm_ring_view(const cm_ctx *ctx, int32_t slot, void **grads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CM_H_ */

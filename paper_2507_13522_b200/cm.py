@@ -1,0 +1,224 @@
+"""Thin ctypes binding of libcm.so (include/cm.h).  Argument marshalling only: every step
+of the path runs in the library's sm_100a kernels.  Names mirror the C ABI.
+
+There is no fallback: if libcm.so is missing or cannot load, importing a Context raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcm.so")
+
+CM_OK, CM_ERR_ARG, CM_ERR_CONFIG, CM_ERR_INVARIANT, CM_ERR_UNRECOVERABLE, CM_ERR_CUDA, CM_ERR_STATE = range(7)
+STATUS_NAMES = {0: "CM_OK", 1: "CM_ERR_ARG", 2: "CM_ERR_CONFIG", 3: "CM_ERR_INVARIANT",
+                4: "CM_ERR_UNRECOVERABLE", 5: "CM_ERR_CUDA", 6: "CM_ERR_STATE"}
+CM_F32, CM_BF16 = 0, 1
+CM_SHADOW_HOST, CM_SHADOW_DEVICE = 0, 1
+CM_FLAG_NO_TAP = 1 << 0
+CM_FLAG_ATTACH = 1 << 1
+CM_FLAG_TAP_COPYENGINE = 1 << 2
+
+# every symbol include/cm.h declares (tests check the library exports all of them)
+EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
+           "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step",
+           "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_get_info",
+           "cm_bucket_info", "cm_shadow_view", "cm_ring_view"]
+
+
+class cm_config(C.Structure):
+    _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32),
+                ("ring_depth", C.c_int32), ("shadow_place", C.c_int32), ("reserved", C.c_int32),
+                ("shm_name", C.c_char_p), ("flags", C.c_uint64)]
+
+
+class cm_layer_table(C.Structure):
+    _fields_ = [("numel", C.POINTER(C.c_int64)), ("n_tensors", C.c_int32), ("grad_dtype", C.c_int32),
+                ("cap_bytes", C.c_int64)]
+
+
+class cm_adamw(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("weight_decay", C.c_double)]
+
+
+class cm_info(C.Structure):
+    _fields_ = [("n_buckets", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
+                ("ring_depth", C.c_int32), ("grad_dtype", C.c_int32), ("shadow_place", C.c_int32),
+                ("peers_in_process", C.c_int32), ("reserved", C.c_int32), ("padded_numel", C.c_int64),
+                ("shard_numel", C.c_int64), ("shadow_step", C.c_int64), ("launches", C.c_int64),
+                ("layout_hash", C.c_uint64)]
+
+
+class CMError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.cm_plan_buckets.argtypes = [C.POINTER(cm_layer_table), C.c_int32, C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        L.cm_init.argtypes = [C.POINTER(cm_config), C.POINTER(P)]
+        L.cm_register_buckets.argtypes = [P, C.POINTER(cm_layer_table), P, P, P, P, P, C.POINTER(C.c_size_t)]
+        L.cm_blob_size.restype = C.c_size_t
+        L.cm_blob_size.argtypes = []
+        L.cm_connect.argtypes = [P, P, C.c_size_t]
+        L.cm_finalize.argtypes = [P]
+        L.cm_unlink_shadow.argtypes = [C.c_char_p, C.c_int32]
+        L.cm_last_error.restype = C.c_char_p
+        L.cm_last_error.argtypes = [P]
+        L.cm_allreduce_multicast.argtypes = [P, C.c_int32, C.c_int64, P]
+        L.cm_apply_step.argtypes = [P, C.c_int64, C.POINTER(cm_adamw), P]
+        L.cm_shadow_apply.argtypes = [P, C.c_int64, P]
+        L.cm_restore.argtypes = [P, C.POINTER(C.c_int64), P]
+        L.cm_gen_grads.argtypes = [P, C.c_uint64, C.c_int64, C.c_int32, P]
+        L.cm_init_state.argtypes = [P, C.c_uint64, P]
+        L.cm_verify.argtypes = [P, C.POINTER(C.c_int64), P]
+        L.cm_get_info.argtypes = [P, C.POINTER(cm_info)]
+        L.cm_bucket_info.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.cm_shadow_view.argtypes = [P, C.c_int32, C.POINTER(P), C.POINTER(P), C.POINTER(P)]
+        L.cm_ring_view.argtypes = [P, C.c_int32, C.POINTER(P)]
+        for name in EXPORTS:
+            if name not in ("cm_blob_size", "cm_last_error"):
+                getattr(L, name).restype = C.c_int     # cm_status
+        _lib = L
+    return _lib
+
+
+def _layer_table(numel, grad_dtype, cap_bytes):
+    arr = (C.c_int64 * len(numel))(*[int(x) for x in numel])
+    t = cm_layer_table(C.cast(arr, C.POINTER(C.c_int64)), len(numel), int(grad_dtype), int(cap_bytes))
+    return t, arr
+
+
+def plan_buckets(numel, grad_dtype, cap_bytes, world_size):
+    """cm_plan_buckets -> (padded_numel, n_buckets, tensor_elem_offset list)."""
+    t, keep = _layer_table(numel, grad_dtype, cap_bytes)
+    tot = C.c_int64(0)
+    nb = C.c_int32(0)
+    offs = (C.c_int64 * max(len(numel), 1))()
+    st = lib().cm_plan_buckets(C.byref(t), int(world_size), C.byref(tot), C.byref(nb), offs)
+    if st != CM_OK:
+        raise CMError(st, "cm_plan_buckets rejected the table")
+    return tot.value, nb.value, list(offs[:len(numel)])
+
+
+def unlink_shadow(name, rank):
+    return lib().cm_unlink_shadow(name.encode(), int(rank))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream   # torch.cuda.Stream
+
+
+class Context:
+    """One cm_ctx (one rank).  Methods mirror the C ABI one to one."""
+
+    def __init__(self, world_size, rank, device, ring_depth=2, shadow_place=CM_SHADOW_HOST,
+                 shm_name="checkmate", flags=0):
+        self._ctx = C.c_void_p()
+        self._name = shm_name.encode() if shm_name else None
+        cfg = cm_config(world_size, rank, device, ring_depth, shadow_place, 0, self._name, flags)
+        st = lib().cm_init(C.byref(cfg), C.byref(self._ctx))
+        if st != CM_OK:
+            msg = self.last_error()
+            self.finalize()
+            raise CMError(st, msg)
+        self._keep = []
+
+    def last_error(self):
+        if not self._ctx:
+            return "no context"
+        return lib().cm_last_error(self._ctx).decode(errors="replace")
+
+    def _check(self, st):
+        if st != CM_OK:
+            raise CMError(st, self.last_error())
+
+    def register_buckets(self, numel, grad_dtype, cap_bytes, grad_ptr, p_ptr, m_ptr, v_ptr) -> bytes:
+        t, arr = _layer_table(numel, grad_dtype, cap_bytes)
+        self._keep.append(arr)
+        cap = lib().cm_blob_size()
+        buf = C.create_string_buffer(cap)
+        blen = C.c_size_t(cap)
+        self._check(lib().cm_register_buckets(self._ctx, C.byref(t), grad_ptr, p_ptr, m_ptr, v_ptr, buf,
+                                              C.byref(blen)))
+        return buf.raw[:blen.value]
+
+    def connect(self, blobs):
+        data = b"".join(blobs)
+        self._check(lib().cm_connect(self._ctx, data, len(blobs[0])))
+
+    def allreduce_multicast(self, bucket, iteration, stream=None):
+        self._check(lib().cm_allreduce_multicast(self._ctx, int(bucket), int(iteration), _stream_ptr(stream)))
+
+    def apply_step(self, step, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, stream=None):
+        hp = cm_adamw(lr, beta1, beta2, eps, weight_decay)
+        self._check(lib().cm_apply_step(self._ctx, int(step), C.byref(hp), _stream_ptr(stream)))
+
+    def shadow_apply(self, step, stream=None):
+        self._check(lib().cm_shadow_apply(self._ctx, int(step), _stream_ptr(stream)))
+
+    def restore(self, stream=None) -> int:
+        out = C.c_int64(-1)
+        self._check(lib().cm_restore(self._ctx, C.byref(out), _stream_ptr(stream)))
+        return out.value
+
+    def gen_grads(self, seed, iteration, scale, stream=None):
+        self._check(lib().cm_gen_grads(self._ctx, int(seed), int(iteration), int(scale), _stream_ptr(stream)))
+
+    def init_state(self, seed, stream=None):
+        self._check(lib().cm_init_state(self._ctx, int(seed), _stream_ptr(stream)))
+
+    def verify(self, stream=None) -> int:
+        out = C.c_int64(-2)
+        st = lib().cm_verify(self._ctx, C.byref(out), _stream_ptr(stream))
+        if st not in (CM_OK, CM_ERR_INVARIANT):
+            self._check(st)
+        return out.value
+
+    def info(self) -> cm_info:
+        i = cm_info()
+        self._check(lib().cm_get_info(self._ctx, C.byref(i)))
+        return i
+
+    def bucket_info(self, b):
+        o, p, u = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(lib().cm_bucket_info(self._ctx, int(b), C.byref(o), C.byref(p), C.byref(u)))
+        return o.value, p.value, u.value
+
+    def shadow_view(self, half):
+        p, m, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        self._check(lib().cm_shadow_view(self._ctx, int(half), C.byref(p), C.byref(m), C.byref(v)))
+        return p.value, m.value, v.value
+
+    def ring_view(self, slot):
+        g = C.c_void_p()
+        self._check(lib().cm_ring_view(self._ctx, int(slot), C.byref(g)))
+        return g.value
+
+    def finalize(self):
+        if self._ctx:
+            lib().cm_finalize(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.finalize()
+        except Exception:
+            pass

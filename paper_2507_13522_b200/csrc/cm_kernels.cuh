@@ -1,0 +1,451 @@
+// cm_kernels.cuh -- sm_100a device code of the Checkmate hot path (arXiv 2507.13522).
+//
+// All kernels are element-local and bandwidth-bound (no tensor cores: nothing on this
+// path is a contraction).  Their rooflines and algorithmic bytes are in
+// DESIGN.md "Kernels".  Included only by cm_runtime.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace cm {
+
+constexpr int kMaxRanks = 8;
+constexpr int kMaxBarrierBlocks = 1024;   // signal-pad slots per region
+constexpr int kPadRegions = 2;            // 0 = entry, 1 = exit
+
+// ------------------------------------------------------------------ memory helpers
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_v4(void* p, const uint4& v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+// streaming (evict-first) variants for data touched once per launch
+__device__ __forceinline__ uint4 ld_cs_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_cs_v4(void* p, const uint4& v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// ------------------------------------------------------------------ cross-GPU barrier
+// Pairwise flag exchange between block j of every rank (the grids of one collective
+// have equal size on all ranks).  pads[k] is rank k's signal pad (peer-mapped); slot
+// (region, block, src) in rank k's pad holds the last epoch src announced to k.
+// Epochs increase by one per collective launch and are identical on all ranks (every
+// rank issues the same sequence of collectives), so a flag can never be satisfied by a
+// stale value; ">=" tolerates a peer that already announced the next epoch.
+struct Pads {
+    uint32_t* p[kMaxRanks];
+};
+__device__ __forceinline__ uint32_t* pad_slot(uint32_t* base, int region, int block, int src) {
+    return base + ((size_t)region * kMaxBarrierBlocks + block) * kMaxRanks + src;
+}
+__device__ __forceinline__ void block_barrier(const Pads& pads, int n, int rank, uint32_t epoch,
+                                              int region) {
+    __syncthreads();   // all of this block's prior stores are ordered before the release
+    if (threadIdx.x < (unsigned)n) {
+        const int k = threadIdx.x;
+        st_release_sys(pad_slot(pads.p[k], region, blockIdx.x, rank), epoch);
+        const uint32_t* mine = pad_slot(pads.p[rank], region, blockIdx.x, k);
+        while ((int)(ld_acquire_sys(mine) - epoch) < 0) {
+        }
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ dtype traits
+// A 16-byte vector of gradients: 4 fp32 or 8 bf16.
+struct F32Tag {};
+struct BF16Tag {};
+template <typename G> struct GT;
+template <> struct GT<F32Tag> {
+    static constexpr int kPerVec = 4;
+    static constexpr int kBytes = 4;
+};
+template <> struct GT<BF16Tag> {
+    static constexpr int kPerVec = 8;
+    static constexpr int kBytes = 2;
+};
+
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+// round-to-nearest-even fp32 -> bf16 (reading R25; finite inputs)
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+    uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
+    return a | (b << 16);
+}
+
+// ------------------------------------------------------------------ counter-based inputs
+// SplitMix64 finaliser; h = sm(K ^ i), K = sm(seed ^ r<<48 ^ t)
+// computed on the host.  fp32: mant int24, value = mant * 2^(-23-e-s); bf16: mant int8,
+// value = mant * 2^(-7-e-s); e = (h>>32)&7.  Exact in the target dtype.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ float pow2i(int k) {   // 2^k for k in the normal range
+    return __uint_as_float((uint32_t)(127 + k) << 23);
+}
+__device__ __forceinline__ float gen_f32(uint64_t K, uint64_t i, int s) {
+    uint64_t h = splitmix64(K ^ i);
+    int e = (int)((h >> 32) & 7u);
+    int mant = (int)(h >> 40) - (1 << 23);
+    return __fmul_rn((float)mant, pow2i(-23 - e - s));
+}
+__device__ __forceinline__ uint32_t gen_bf16bits(uint64_t K, uint64_t i, int s) {
+    uint64_t h = splitmix64(K ^ i);
+    int e = (int)((h >> 32) & 7u);
+    int mant = (int)(h >> 56) - 128;
+    return __float_as_uint(__fmul_rn((float)mant, pow2i(-7 - e - s))) >> 16;
+}
+
+struct BucketDev {
+    int64_t off;      // flat element offset
+    int64_t padded;   // E_b
+    int64_t used;     // real elements (rest is zero padding)
+    int64_t shard_off;// shard-local element offset = off / n
+};
+
+// Grid-stride over 16-byte vectors of the flat buffer; a running bucket index locates
+// padding (buckets are whole vectors, so a vector never straddles two buckets).
+template <typename G>
+__global__ void __launch_bounds__(256) gen_grads_kernel(void* __restrict__ out, int64_t nvec,
+                                                        const BucketDev* __restrict__ buckets,
+                                                        int nb, uint64_t K, int s) {
+    constexpr int V = GT<G>::kPerVec;
+    int b = 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nvec;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = q * V;
+        while (b + 1 < nb && i0 >= buckets[b + 1].off) ++b;
+        const int64_t lim = buckets[b].off + buckets[b].used;
+        uint32_t w[4];
+        if constexpr (V == 4) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                w[k] = (i0 + k < lim) ? __float_as_uint(gen_f32(K, (uint64_t)(i0 + k), s)) : 0u;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t lo = (i0 + 2 * k < lim) ? gen_bf16bits(K, (uint64_t)(i0 + 2 * k), s) : 0u;
+                uint32_t hi = (i0 + 2 * k + 1 < lim) ? gen_bf16bits(K, (uint64_t)(i0 + 2 * k + 1), s) : 0u;
+                w[k] = lo | (hi << 16);
+            }
+        }
+        st_v4((char*)out + q * 16, make_uint4(w[0], w[1], w[2], w[3]));
+    }
+}
+
+// p = p_0 (generator, rank 0xFFFF, t 0, s 0, times 2^-5), m = v = 0.
+__global__ void __launch_bounds__(256) init_state_kernel(float* __restrict__ p, float* __restrict__ m,
+                                                         float* __restrict__ v, int64_t nvec,
+                                                         const BucketDev* __restrict__ buckets, int nb,
+                                                         uint64_t K) {
+    int b = 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nvec;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = q * 4;
+        while (b + 1 < nb && i0 >= buckets[b + 1].off) ++b;
+        const int64_t lim = buckets[b].off + buckets[b].used;
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            w[k] = (i0 + k < lim) ? __float_as_uint(__fmul_rn(gen_f32(K, (uint64_t)(i0 + k), 0), 0.03125f)) : 0u;
+        st_v4(p + i0, make_uint4(w[0], w[1], w[2], w[3]));
+        st_v4(m + i0, make_uint4(0, 0, 0, 0));
+        st_v4(v + i0, make_uint4(0, 0, 0, 0));
+    }
+}
+
+// ------------------------------------------------------------------ RS + tap + AG
+// One launch per (bucket, iteration) per rank.  Rank r reduces shard r of the bucket:
+// for every 16-byte vector of the shard, read it from all n ranks' grad buffers (n-1 of
+// them over NVLink), sum in rank order in fp32 registers (seeded with rank 0's value,
+// readings R2/R3), round once to bf16 for bf16 grads (R14), then store the same
+// registers to (a) the host ring (the tap, exactly once box-wide) and (b) shard r of all
+// n ranks' grad buffers (the all-gather).  In place is race-free: rank r is the only
+// rank that reads or writes shard r of any buffer, and a thread writes an element only
+// after it has read that element from all n ranks.
+struct ArParams {
+    char* buf[kMaxRanks];   // grad buffer of rank k + bucket byte offset + shard byte offset
+    char* tap;              // host-mapped ring slot + shard byte offset (nullptr: no tap)
+    int64_t nvec;           // 16-byte vectors in the shard
+    Pads pads;
+    uint32_t epoch;
+    int rank;
+    int barriers;           // 0 when all ranks live in this process (virtual ranks)
+    int ag;                 // 0 when n == 1 (the reduced value equals the local value)
+    unsigned long long* done_ctr;  // device counter: last block to finish publishes the flag
+    unsigned long long done_target;
+    volatile uint64_t* tap_flag;   // host-mapped (slot, bucket, rank) flag; nullptr: none
+    uint64_t tap_flag_value;       // iteration + 1
+};
+
+template <typename G, int N>
+__device__ __forceinline__ uint4 reduce_vec(const uint4 (&x)[N]) {
+    if constexpr (std::is_same<G, F32Tag>::value) {
+        float a0 = __uint_as_float(x[0].x), a1 = __uint_as_float(x[0].y);
+        float a2 = __uint_as_float(x[0].z), a3 = __uint_as_float(x[0].w);
+#pragma unroll
+        for (int k = 1; k < N; ++k) {
+            a0 = __fadd_rn(a0, __uint_as_float(x[k].x));
+            a1 = __fadd_rn(a1, __uint_as_float(x[k].y));
+            a2 = __fadd_rn(a2, __uint_as_float(x[k].z));
+            a3 = __fadd_rn(a3, __uint_as_float(x[k].w));
+        }
+        return make_uint4(__float_as_uint(a0), __float_as_uint(a1), __float_as_uint(a2),
+                          __float_as_uint(a3));
+    } else {
+        if constexpr (N == 1) return x[0];   // RNE(upcast(b)) == b
+        float a[8];
+        a[0] = bf16lo(x[0].x); a[1] = bf16hi(x[0].x); a[2] = bf16lo(x[0].y); a[3] = bf16hi(x[0].y);
+        a[4] = bf16lo(x[0].z); a[5] = bf16hi(x[0].z); a[6] = bf16lo(x[0].w); a[7] = bf16hi(x[0].w);
+#pragma unroll
+        for (int k = 1; k < N; ++k) {
+            a[0] = __fadd_rn(a[0], bf16lo(x[k].x)); a[1] = __fadd_rn(a[1], bf16hi(x[k].x));
+            a[2] = __fadd_rn(a[2], bf16lo(x[k].y)); a[3] = __fadd_rn(a[3], bf16hi(x[k].y));
+            a[4] = __fadd_rn(a[4], bf16lo(x[k].z)); a[5] = __fadd_rn(a[5], bf16hi(x[k].z));
+            a[6] = __fadd_rn(a[6], bf16lo(x[k].w)); a[7] = __fadd_rn(a[7], bf16hi(x[k].w));
+        }
+        return make_uint4(pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3]), pack_bf16x2(a[4], a[5]),
+                          pack_bf16x2(a[6], a[7]));
+    }
+}
+
+constexpr int kArThreads = 512;
+constexpr int kArUnroll = 2;
+
+template <typename G, int N>
+__global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P) {
+    if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 0);   // peers' grads are ready
+
+    const int64_t stride = (int64_t)gridDim.x * kArThreads;
+    int64_t q = blockIdx.x * (int64_t)kArThreads + threadIdx.x;
+    for (; q + (kArUnroll - 1) * stride < P.nvec; q += kArUnroll * stride) {
+        uint4 x[kArUnroll][N];
+#pragma unroll
+        for (int u = 0; u < kArUnroll; ++u)
+#pragma unroll
+            for (int k = 0; k < N; ++k) x[u][k] = ld_v4(P.buf[k] + (q + u * stride) * 16);
+#pragma unroll
+        for (int u = 0; u < kArUnroll; ++u) {
+            const uint4 r = reduce_vec<G, N>(x[u]);
+            const int64_t off = (q + u * stride) * 16;
+            if (P.tap) st_cs_v4(P.tap + off, r);
+            if (P.ag) {
+#pragma unroll
+                for (int k = 0; k < N; ++k) st_v4(P.buf[k] + off, r);
+            }
+        }
+    }
+    for (; q < P.nvec; q += stride) {
+        uint4 x[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) x[k] = ld_v4(P.buf[k] + q * 16);
+        const uint4 r = reduce_vec<G, N>(x);
+        if (P.tap) st_cs_v4(P.tap + q * 16, r);
+        if (P.ag) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) st_v4(P.buf[k] + q * 16, r);
+        }
+    }
+
+    if (P.tap_flag) {
+        // every tap store of this block is visible system-wide before the block is
+        // counted; the last block publishes the (slot, bucket, rank) flag for restore
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long prev = atomicAdd(P.done_ctr, 1ull);
+            if (prev + 1 == P.done_target) {
+                __threadfence_system();
+                *P.tap_flag = P.tap_flag_value;
+            }
+        }
+    }
+    if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 1);   // bucket complete everywhere
+}
+
+// ------------------------------------------------------------------ AdamW
+// Canonical fp32 op sequence (reading R4), each op IEEE round-to-nearest, no FMA:
+//   g = R*inv_n; m = B1*m + c1*g; v = B2*v + c2*(g*g); mh = m/bc1; vh = v/bc2;
+//   d = sqrt(vh) + eps; p = p - lr*(mh/d + wd*p)
+struct AdamScalars {
+    float c1, c2, B1, B2, bc1, bc2, inv_n, lr, eps, wd;
+};
+
+__device__ __forceinline__ void adamw_elem(float R, const AdamScalars& s, float& p, float& m, float& v) {
+    const float g = __fmul_rn(R, s.inv_n);
+    const float mm = __fadd_rn(__fmul_rn(s.B1, m), __fmul_rn(s.c1, g));
+    const float vv = __fadd_rn(__fmul_rn(s.B2, v), __fmul_rn(s.c2, __fmul_rn(g, g)));
+    const float mh = __fdiv_rn(mm, s.bc1);
+    const float vh = __fdiv_rn(vv, s.bc2);
+    const float d = __fadd_rn(__fsqrt_rn(vh), s.eps);
+    const float upd = __fadd_rn(__fdiv_rn(mh, d), __fmul_rn(s.wd, p));
+    p = __fsub_rn(p, __fmul_rn(s.lr, upd));
+    m = mm;
+    v = vv;
+}
+
+// A work item = 8 consecutive elements (two float4 of state; 32 B of fp32 grads or 16 B
+// of bf16 grads).  All arrays are 16-byte aligned and a multiple of 8 elements long
+// except possibly a 4-element tail for fp32 (handled by the tail item path).
+// In/out arrays may alias (training: in place) or not (shadow: ping-pong halves).
+struct AdamParams {
+    const void* g;
+    const float* p_in; const float* m_in; const float* v_in;
+    float* p_out; float* m_out; float* v_out;
+    int64_t n;          // elements (multiple of 4)
+    AdamScalars s;
+    volatile float* hp_rec;        // host-mapped ring-slot scalar record (or nullptr)
+    volatile int64_t* hp_tag;      // written after the record: the step
+    int64_t step;
+};
+
+constexpr int kAdamThreads = 256;
+
+template <typename G>
+__device__ __forceinline__ void adamw_item(const AdamParams& P, int64_t e) {
+    // e: first element of the 8-element item (e + 8 <= n).  __ldcs/__stcs: evict-first
+    // streaming accesses (every byte is touched once per launch).
+    float4 g0, g1;
+    if constexpr (std::is_same<G, F32Tag>::value) {
+        g0 = __ldcs(reinterpret_cast<const float4*>((const float*)P.g + e));
+        g1 = __ldcs(reinterpret_cast<const float4*>((const float*)P.g + e + 4));
+    } else {
+        const uint4 gb = __ldcs(reinterpret_cast<const uint4*>((const uint16_t*)P.g + e));
+        g0 = make_float4(bf16lo(gb.x), bf16hi(gb.x), bf16lo(gb.y), bf16hi(gb.y));
+        g1 = make_float4(bf16lo(gb.z), bf16hi(gb.z), bf16lo(gb.w), bf16hi(gb.w));
+    }
+    float4 p0 = __ldcs(reinterpret_cast<const float4*>(P.p_in + e));
+    float4 p1 = __ldcs(reinterpret_cast<const float4*>(P.p_in + e + 4));
+    float4 m0 = __ldcs(reinterpret_cast<const float4*>(P.m_in + e));
+    float4 m1 = __ldcs(reinterpret_cast<const float4*>(P.m_in + e + 4));
+    float4 v0 = __ldcs(reinterpret_cast<const float4*>(P.v_in + e));
+    float4 v1 = __ldcs(reinterpret_cast<const float4*>(P.v_in + e + 4));
+    adamw_elem(g0.x, P.s, p0.x, m0.x, v0.x); adamw_elem(g0.y, P.s, p0.y, m0.y, v0.y);
+    adamw_elem(g0.z, P.s, p0.z, m0.z, v0.z); adamw_elem(g0.w, P.s, p0.w, m0.w, v0.w);
+    adamw_elem(g1.x, P.s, p1.x, m1.x, v1.x); adamw_elem(g1.y, P.s, p1.y, m1.y, v1.y);
+    adamw_elem(g1.z, P.s, p1.z, m1.z, v1.z); adamw_elem(g1.w, P.s, p1.w, m1.w, v1.w);
+    __stcs(reinterpret_cast<float4*>(P.p_out + e), p0);
+    __stcs(reinterpret_cast<float4*>(P.p_out + e + 4), p1);
+    __stcs(reinterpret_cast<float4*>(P.m_out + e), m0);
+    __stcs(reinterpret_cast<float4*>(P.m_out + e + 4), m1);
+    __stcs(reinterpret_cast<float4*>(P.v_out + e), v0);
+    __stcs(reinterpret_cast<float4*>(P.v_out + e + 4), v1);
+}
+
+template <typename G>
+__global__ void __launch_bounds__(kAdamThreads) adamw_kernel(const AdamParams P) {
+    const int64_t items = P.n / 8;
+    const int64_t stride = (int64_t)gridDim.x * kAdamThreads;
+    int64_t q = blockIdx.x * (int64_t)kAdamThreads + threadIdx.x;
+    for (; q + stride < items; q += 2 * stride) {
+        adamw_item<G>(P, q * 8);
+        adamw_item<G>(P, (q + stride) * 8);
+    }
+    for (; q < items; q += stride) adamw_item<G>(P, q * 8);
+    // fp32 tail of 4 elements (n % 8 == 4)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (P.n & 7)) {
+        for (int64_t e = items * 8; e < P.n; ++e) {
+            float R;
+            if constexpr (std::is_same<G, F32Tag>::value) R = ((const float*)P.g)[e];
+            else R = __uint_as_float(((uint32_t)((const uint16_t*)P.g)[e]) << 16);
+            float p = P.p_in[e], m = P.m_in[e], v = P.v_in[e];
+            adamw_elem(R, P.s, p, m, v);
+            P.p_out[e] = p; P.m_out[e] = m; P.v_out[e] = v;
+        }
+    }
+    if (P.hp_rec && blockIdx.x == 0 && threadIdx.x == 0) {
+        const float* sf = &P.s.c1;
+        for (int k = 0; k < 10; ++k) P.hp_rec[k] = sf[k];
+        __threadfence_system();
+        *P.hp_tag = P.step;
+    }
+}
+
+// ------------------------------------------------------------------ shard gather/scatter
+// Shard-local index j of rank r <-> flat index off_b + r*E_b/n + (j - shard_off_b).
+// dir 0 (snapshot): flat device p/m/v of this rank -> shard-local dst arrays.
+// dir 1 (restore):  shard-local src arrays -> flat p/m/v of all ranks (all-gather).
+struct ShardCopyParams {
+    const float* src[3];
+    float* dst[3][kMaxRanks];   // dir 1: per-rank flat buffers; dir 0: [k][0] shard-local
+    const BucketDev* buckets;
+    int nb, n, rank, dir, barriers;
+    int64_t shard_nvec;         // shard-local 16-byte vectors of fp32
+    Pads pads;
+    uint32_t epoch;
+};
+
+__global__ void __launch_bounds__(256) shard_copy_kernel(const ShardCopyParams P) {
+    if (P.dir == 1 && P.barriers) block_barrier(P.pads, P.n, P.rank, P.epoch, 0);
+    int b = 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P.shard_nvec;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = q * 4;
+        while (b + 1 < P.nb && j >= P.buckets[b + 1].shard_off) ++b;
+        const BucketDev B = P.buckets[b];
+        const int64_t flat = B.off + (int64_t)P.rank * (B.padded / P.n) + (j - B.shard_off);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (P.dir == 0) {
+                st_v4(P.dst[a][0] + j, ld_v4(P.src[a] + flat));
+            } else {
+                const uint4 x = ld_v4(P.src[a] + j);
+                for (int k = 0; k < P.n; ++k) st_v4(P.dst[a][k] + flat, x);
+            }
+        }
+    }
+    if (P.dir == 1 && P.barriers) block_barrier(P.pads, P.n, P.rank, P.epoch, 1);
+}
+
+// bitwise compare shadow shard-local arrays with this rank's flat shard
+__global__ void __launch_bounds__(256) compare_kernel(const float* __restrict__ sp, const float* __restrict__ sm,
+                                                      const float* __restrict__ sv, const float* __restrict__ p,
+                                                      const float* __restrict__ m, const float* __restrict__ v,
+                                                      const BucketDev* __restrict__ buckets, int nb, int n,
+                                                      int rank, int64_t shard_n,
+                                                      unsigned long long* first_bad) {
+    int b = 0;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < shard_n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        while (b + 1 < nb && j >= buckets[b + 1].shard_off) ++b;
+        const BucketDev B = buckets[b];
+        const int64_t flat = B.off + (int64_t)rank * (B.padded / n) + (j - B.shard_off);
+        if (__float_as_uint(sp[j]) != __float_as_uint(p[flat]) ||
+            __float_as_uint(sm[j]) != __float_as_uint(m[flat]) ||
+            __float_as_uint(sv[j]) != __float_as_uint(v[flat]))
+            atomicMin(first_bad, (unsigned long long)flat);
+    }
+}
+
+// stream-ordered store of one int64 into host-mapped memory (segment header)
+__global__ void publish_kernel(volatile int64_t* dst, int64_t value) {
+    __threadfence_system();
+    *dst = value;
+    __threadfence_system();
+}
+
+}  // namespace cm

@@ -1,0 +1,1037 @@
+// cm_runtime.cu -- host runtime and C ABI of libcm.so (see include/cm.h for the contract).
+//
+// One context per rank.  Responsibilities: bucket planning, peer
+// mapping over CUDA IPC (NVLink), the POSIX-shm shadow segment (tap ring + shadow state,
+// the analog of the paper's shadow cluster), stream/event
+// orchestration for flow control, and kernel launches.  Every
+// numerical step runs in the sm_100a kernels of cm_kernels.cuh; this file only moves
+// pointers, computes the per-step fp32 scalars (reading R5/R6) and sequences work.
+#include "cm.h"
+#include "cm_kernels.cuh"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+using namespace cm;
+
+// ====================================================================== segment layout
+// One POSIX shm segment per rank: "/<name>.r<rank>".
+//   [0, 4096)          SegHeader
+//   slot meta          D x SlotMeta (the step scalars recorded for the shadow / roll-forward)
+//   flags              D x n_buckets x uint64 (tap flag: iteration+1 once the shard is in)
+//   ring               D x shard_numel x sizeof(G)    (the tap ring, shard-local layout)
+//   state (HOST)       2 halves x {p, m, v} x shard_numel fp32 (ping-pong shadow state)
+namespace {
+
+constexpr uint64_t kMagic = 0x434B4D5442323030ull;  // "CKMTB200"
+constexpr uint32_t kVersion = 1;
+constexpr size_t kAlign = 4096;
+
+struct SegHeader {
+    uint64_t magic;
+    uint32_t version;
+    int32_t world_size, rank, dtype, ring_depth, n_buckets, shadow_place, pad0;
+    int64_t shard_numel;
+    uint64_t layout_hash;
+    volatile int64_t shadow_step;   // last step published by the shadow
+    volatile int64_t half_step[2];  // step held by each ping-pong half, -1 = invalid
+    uint64_t meta_off, flags_off, ring_off, state_off, total;
+};
+static_assert(sizeof(SegHeader) <= kAlign, "header");
+
+struct SlotMeta {
+    volatile int64_t step_tag;  // step whose scalars follow (written after them)
+    volatile float sc[10];
+    int32_t pad[4];
+};
+static_assert(sizeof(SlotMeta) == 64, "meta");
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+uint64_t fnv1a(uint64_t h, const void* data, size_t n) {
+    const unsigned char* p = (const unsigned char*)data;
+    for (size_t i = 0; i < n; ++i) { h ^= p[i]; h *= 0x100000001B3ull; }
+    return h;
+}
+
+uint64_t process_token() {
+    static uint64_t tok = [] {
+        std::random_device rd;
+        return ((uint64_t)rd() << 32) ^ rd() ^ ((uint64_t)getpid() << 16);
+    }();
+    return tok;
+}
+
+// Exchange blob: what a rank tells its peers.
+struct Blob {
+    uint64_t magic;
+    uint64_t token;         // process identity: equal tokens = same process
+    int32_t world_size, rank, device, dtype;
+    uint64_t layout_hash;
+    int64_t padded_numel;
+    // 0 grad, 1 p, 2 m, 3 v, 4 signal pad
+    cudaIpcMemHandle_t handle[5];
+    uint64_t base[5];       // allocation base address in the owner (dedupe key)
+    uint64_t offset[5];     // pointer - base
+    uint64_t raw[5];        // raw pointer (usable in-process)
+};
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+}  // namespace
+
+struct cm_ctx {
+    cm_config cfg{};
+    std::string shm_name;
+    std::string err;
+    int n = 1, rank = 0, dev = 0, D = 2, dtype = 0, es = 4;
+    bool no_tap = false, attach = false, ce_tap = false;
+    int shadow_place = CM_SHADOW_HOST;
+    int sms = 148;
+    bool cuda_dead = false;
+
+    // plan
+    bool registered = false, connected = false;
+    std::vector<int64_t> numel;
+    int64_t cap_bytes = 0;
+    std::vector<BucketDev> buckets;
+    int64_t P_pad = 0, shard_numel = 0;
+    uint64_t layout_hash = 0;
+    BucketDev* d_buckets = nullptr;
+
+    // user buffers (this rank) and peers
+    void* grad = nullptr;
+    float *p = nullptr, *m = nullptr, *v = nullptr;
+    uint32_t* pad = nullptr;
+    char* peer_grad[kMaxRanks] = {};
+    float* peer_p[kMaxRanks] = {};
+    float* peer_m[kMaxRanks] = {};
+    float* peer_v[kMaxRanks] = {};
+    Pads pads{};
+    std::vector<std::pair<uint64_t, void*>> opened;  // (peer base key, mapped ptr)
+    bool in_process = false, barriers = true;
+    uint32_t epoch = 0;
+    unsigned long long* d_done_ctr = nullptr;
+    unsigned long long done_total = 0;
+    unsigned long long* d_bad = nullptr;
+
+    // launch geometry
+    int ar_blocks_max = 296, adam_blocks = 1184, shadow_blocks = 296, misc_blocks = 1184;
+
+    // shadow segment
+    int shm_fd = -1;
+    char* seg = nullptr;
+    size_t seg_size = 0;
+    bool seg_registered = false;
+    char* seg_dev = nullptr;      // device alias of the mapped segment
+    SegHeader* hdr = nullptr;
+    float* state_dev_alloc = nullptr;   // DEVICE placement halves
+    float* st[2][3] = {};               // host-visible pointers of halves (HOST) / device (DEVICE)
+    float* st_dev[2][3] = {};           // device-usable pointers of halves
+
+    // iteration bookkeeping
+    int64_t cur_iter = 0;
+    std::vector<char> issued;
+    int issued_count = 0;
+    int64_t train_step = 0;
+    int64_t shadow_enq = 0;
+    std::vector<AdamScalars> slot_sc;
+    std::vector<int64_t> slot_sc_step;
+    std::vector<cudaEvent_t> ev_tap_done, ev_slot_free;
+
+    // scalar cache (reading R6: beta^s by repeated multiplication from 1.0)
+    double pw_b1 = 1.0, pw_b2 = 1.0, pw_beta1 = -1, pw_beta2 = -1;
+    int64_t pw_s = 0;
+
+    int64_t launches = 0;
+};
+
+// ====================================================================== helpers
+static cm_status fail(cm_ctx* c, cm_status s, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    if (c && s == CM_ERR_CUDA) c->cuda_dead = true;
+    return s;
+}
+
+#define CU(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(c, CM_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                              \
+    } while (0)
+
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+// ---------------------------------------------------------------- bucket planner
+// PAPER.md:258-264 (sec 4.2.2) with readings R10-R13 (see cm.h cm_plan_buckets).
+struct PlanOut {
+    std::vector<BucketDev> buckets;
+    std::vector<int64_t> tensor_off;
+    int64_t total = 0;
+};
+
+static bool plan(const int64_t* numel, int nt, int64_t cap, int es, int n, PlanOut& out) {
+    if (nt <= 0 || cap <= 0 || n <= 0 || (es != 2 && es != 4)) return false;
+    for (int i = 0; i < nt; ++i)
+        if (numel[i] <= 0) return false;
+    const int64_t quantum = (16 / es) * (int64_t)n;
+    std::vector<std::vector<int>> groups;
+    int64_t open_bytes = -1;  // -1: no open bucket
+    for (int i = nt - 1; i >= 0; --i) {
+        const int64_t bytes = numel[i] * es;
+        if (bytes > cap) {
+            groups.push_back({i});
+            open_bytes = -1;
+        } else if (open_bytes >= 0 && open_bytes + bytes <= cap) {
+            groups.back().push_back(i);
+            open_bytes += bytes;
+        } else {
+            groups.push_back({i});
+            open_bytes = bytes;
+        }
+    }
+    out.tensor_off.assign(nt, 0);
+    out.buckets.clear();
+    int64_t flat = 0;
+    for (auto& g : groups) {
+        BucketDev b{};
+        b.off = flat;
+        int64_t used = 0;
+        for (int i : g) {
+            out.tensor_off[i] = flat + used;
+            used += numel[i];
+        }
+        b.used = used;
+        b.padded = (used + quantum - 1) / quantum * quantum;
+        b.shard_off = flat / n;
+        out.buckets.push_back(b);
+        flat += b.padded;
+    }
+    out.total = flat;
+    return true;
+}
+
+// ---------------------------------------------------------------- AdamW scalars
+// Reading R5: fp64 arithmetic, one rounding to fp32 per scalar; R6: beta^s by s
+// repeated fp64 multiplications from 1.0 (cached incrementally: the same sequence).
+static AdamScalars make_scalars(cm_ctx* c, int64_t s, const cm_adamw& hp) {
+    if (hp.beta1 != c->pw_beta1 || hp.beta2 != c->pw_beta2 || s < c->pw_s) {
+        c->pw_b1 = 1.0; c->pw_b2 = 1.0; c->pw_s = 0;
+        c->pw_beta1 = hp.beta1; c->pw_beta2 = hp.beta2;
+    }
+    while (c->pw_s < s) {
+        c->pw_b1 = c->pw_b1 * hp.beta1;
+        c->pw_b2 = c->pw_b2 * hp.beta2;
+        c->pw_s++;
+    }
+    AdamScalars a;
+    a.c1 = (float)(1.0 - hp.beta1);
+    a.c2 = (float)(1.0 - hp.beta2);
+    a.B1 = (float)hp.beta1;
+    a.B2 = (float)hp.beta2;
+    a.bc1 = (float)(1.0 - c->pw_b1);
+    a.bc2 = (float)(1.0 - c->pw_b2);
+    a.inv_n = (float)(1.0 / (double)c->n);
+    a.lr = (float)hp.lr;
+    a.eps = (float)hp.eps;
+    a.wd = (float)hp.weight_decay;
+    return a;
+}
+
+// ---------------------------------------------------------------- launch helpers
+template <typename G>
+static int ar_occupancy() {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rs_tap_ag_kernel<G, 8>, kArThreads, 0);
+    return occ > 0 ? occ : 1;
+}
+
+template <typename G>
+static void launch_ar_t(int n, dim3 grid, cudaStream_t s, const ArParams& P) {
+    switch (n) {
+        case 1: rs_tap_ag_kernel<G, 1><<<grid, kArThreads, 0, s>>>(P); break;
+        case 2: rs_tap_ag_kernel<G, 2><<<grid, kArThreads, 0, s>>>(P); break;
+        case 3: rs_tap_ag_kernel<G, 3><<<grid, kArThreads, 0, s>>>(P); break;
+        case 4: rs_tap_ag_kernel<G, 4><<<grid, kArThreads, 0, s>>>(P); break;
+        case 5: rs_tap_ag_kernel<G, 5><<<grid, kArThreads, 0, s>>>(P); break;
+        case 6: rs_tap_ag_kernel<G, 6><<<grid, kArThreads, 0, s>>>(P); break;
+        case 7: rs_tap_ag_kernel<G, 7><<<grid, kArThreads, 0, s>>>(P); break;
+        default: rs_tap_ag_kernel<G, 8><<<grid, kArThreads, 0, s>>>(P); break;
+    }
+}
+
+static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaStream_t s) {
+    int64_t items = P.n / 8;
+    int64_t want = (items + kAdamThreads - 1) / kAdamThreads;
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, blocks));
+    if (c->dtype == CM_F32) adamw_kernel<F32Tag><<<grid, kAdamThreads, 0, s>>>(P);
+    else adamw_kernel<BF16Tag><<<grid, kAdamThreads, 0, s>>>(P);
+    c->launches++;
+    CHECK_LAUNCH();
+    return CM_OK;
+}
+
+static cm_status publish(cm_ctx* c, volatile int64_t* host_field, int64_t value, cudaStream_t s) {
+    // device alias of a header field
+    volatile int64_t* d = (volatile int64_t*)(c->seg_dev + ((char*)host_field - c->seg));
+    publish_kernel<<<1, 1, 0, s>>>(d, value);
+    c->launches++;
+    CHECK_LAUNCH();
+    return CM_OK;
+}
+
+static SlotMeta* slot_meta(cm_ctx* c, int slot) {
+    return (SlotMeta*)(c->seg + c->hdr->meta_off) + slot;
+}
+static volatile uint64_t* slot_flags(cm_ctx* c, int slot) {
+    return (volatile uint64_t*)(c->seg + c->hdr->flags_off) + (size_t)slot * c->buckets.size();
+}
+static char* ring_slot_dev(cm_ctx* c, int slot) {
+    return c->seg_dev + c->hdr->ring_off + (size_t)slot * c->shard_numel * c->es;
+}
+static char* ring_slot_host(cm_ctx* c, int slot) {
+    return c->seg + c->hdr->ring_off + (size_t)slot * c->shard_numel * c->es;
+}
+template <typename T>
+static T* to_dev(cm_ctx* c, T* host) {
+    return (T*)(c->seg_dev + ((char*)host - c->seg));
+}
+
+// ====================================================================== C ABI
+extern "C" {
+
+size_t cm_blob_size(void) { return sizeof(Blob); }
+
+const char* cm_last_error(const cm_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+cm_status cm_plan_buckets(const cm_layer_table* t, int32_t world_size, int64_t* out_padded,
+                          int32_t* out_nb, int64_t* tensor_off) {
+    if (!t || !t->numel || !out_padded || !out_nb) return CM_ERR_ARG;
+    if (t->grad_dtype != CM_F32 && t->grad_dtype != CM_BF16) return CM_ERR_CONFIG;
+    if (world_size < 1 || world_size > kMaxRanks) return CM_ERR_CONFIG;
+    PlanOut po;
+    if (!plan(t->numel, t->n_tensors, t->cap_bytes, t->grad_dtype == CM_F32 ? 4 : 2, world_size, po))
+        return CM_ERR_CONFIG;
+    *out_padded = po.total;
+    *out_nb = (int32_t)po.buckets.size();
+    if (tensor_off) memcpy(tensor_off, po.tensor_off.data(), sizeof(int64_t) * t->n_tensors);
+    return CM_OK;
+}
+
+cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
+    if (!cfg || !out) return CM_ERR_ARG;
+    *out = nullptr;
+    if (cfg->world_size < 1 || cfg->world_size > kMaxRanks) return CM_ERR_CONFIG;
+    if (cfg->rank < 0 || cfg->rank >= cfg->world_size) return CM_ERR_CONFIG;
+    if (cfg->ring_depth < 2 || cfg->ring_depth > 64) return CM_ERR_CONFIG;
+    if (cfg->shadow_place != CM_SHADOW_HOST && cfg->shadow_place != CM_SHADOW_DEVICE) return CM_ERR_CONFIG;
+    const bool no_tap = (cfg->flags & CM_FLAG_NO_TAP) != 0;
+    if (!no_tap && (!cfg->shm_name || !cfg->shm_name[0] || strlen(cfg->shm_name) > 200))
+        return CM_ERR_CONFIG;
+    cm_ctx* c = new cm_ctx();
+    c->cfg = *cfg;
+    c->shm_name = cfg->shm_name ? cfg->shm_name : "";
+    c->cfg.shm_name = nullptr;
+    c->n = cfg->world_size;
+    c->rank = cfg->rank;
+    c->dev = cfg->device;
+    c->D = cfg->ring_depth;
+    c->no_tap = no_tap;
+    c->attach = (cfg->flags & CM_FLAG_ATTACH) != 0;
+    c->ce_tap = (cfg->flags & CM_FLAG_TAP_COPYENGINE) != 0;
+    c->shadow_place = cfg->shadow_place;
+    *out = c;   // returned even on failure so cm_last_error works; caller finalizes
+
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (c->dev < 0 || c->dev >= ndev) return fail(c, CM_ERR_CONFIG, "device %d not present (%d)", c->dev, ndev);
+    CU(cudaSetDevice(c->dev));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, c->dev));
+    if (prop.major < 10)
+        return fail(c, CM_ERR_CONFIG, "device %d is sm_%d%d; libcm is built for sm_100a", c->dev, prop.major,
+                    prop.minor);
+    c->sms = prop.multiProcessorCount;
+    // signal pad: 2 regions x kMaxBarrierBlocks x kMaxRanks epochs, zero = never signalled
+    const size_t pad_bytes = (size_t)kPadRegions * kMaxBarrierBlocks * kMaxRanks * sizeof(uint32_t);
+    CU(cudaMalloc(&c->pad, pad_bytes));
+    CU(cudaMemset(c->pad, 0, pad_bytes));
+    CU(cudaMalloc(&c->d_done_ctr, sizeof(unsigned long long)));
+    CU(cudaMemset(c->d_done_ctr, 0, sizeof(unsigned long long)));
+    CU(cudaMalloc(&c->d_bad, sizeof(unsigned long long)));
+    for (int i = 0; i < c->D; ++i) {
+        cudaEvent_t a, b;
+        CU(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        c->ev_tap_done.push_back(a);
+        c->ev_slot_free.push_back(b);
+    }
+    c->slot_sc.assign(c->D, AdamScalars{});
+    c->slot_sc_step.assign(c->D, -1);
+    return CM_OK;
+}
+
+cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, float* p, float* m, float* v,
+                              void* blob_out, size_t* blob_len) {
+    if (!c) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (c->registered) return fail(c, CM_ERR_STATE, "already registered");
+    if (!t || !t->numel || !grad || !p || !m || !v || !blob_out || !blob_len)
+        return fail(c, CM_ERR_ARG, "null argument");
+    if (((uintptr_t)grad | (uintptr_t)p | (uintptr_t)m | (uintptr_t)v) & 15)
+        return fail(c, CM_ERR_ARG, "buffers must be 16-byte aligned");
+    if (*blob_len < sizeof(Blob)) return fail(c, CM_ERR_ARG, "blob buffer too small");
+    if (t->grad_dtype != CM_F32 && t->grad_dtype != CM_BF16) return fail(c, CM_ERR_CONFIG, "bad dtype");
+    c->dtype = t->grad_dtype;
+    c->es = c->dtype == CM_F32 ? 4 : 2;
+    PlanOut po;
+    if (!plan(t->numel, t->n_tensors, t->cap_bytes, c->es, c->n, po))
+        return fail(c, CM_ERR_CONFIG, "invalid layer table (empty, non-positive sizes or cap)");
+    if ((int64_t)po.buckets.size() > (1 << 20)) return fail(c, CM_ERR_CONFIG, "too many buckets");
+    c->buckets = po.buckets;
+    c->P_pad = po.total;
+    c->shard_numel = po.total / c->n;
+    c->numel.assign(t->numel, t->numel + t->n_tensors);
+    c->cap_bytes = t->cap_bytes;
+    uint64_t h = 0xCBF29CE484222325ull;
+    h = fnv1a(h, c->numel.data(), c->numel.size() * sizeof(int64_t));
+    h = fnv1a(h, &c->cap_bytes, sizeof c->cap_bytes);
+    h = fnv1a(h, &c->dtype, sizeof c->dtype);
+    h = fnv1a(h, &c->n, sizeof c->n);
+    c->layout_hash = h;
+    c->grad = grad; c->p = p; c->m = m; c->v = v;
+    CU(cudaSetDevice(c->dev));
+    CU(cudaMalloc(&c->d_buckets, sizeof(BucketDev) * c->buckets.size()));
+    CU(cudaMemcpy(c->d_buckets, c->buckets.data(), sizeof(BucketDev) * c->buckets.size(),
+                  cudaMemcpyHostToDevice));
+
+    // launch geometry (identical on every rank: same GPU model, same plan)
+    int occ = c->dtype == CM_F32 ? ar_occupancy<F32Tag>() : ar_occupancy<BF16Tag>();
+    c->ar_blocks_max = std::min(c->sms * occ, kMaxBarrierBlocks);
+    int aocc = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&aocc, adamw_kernel<F32Tag>, kAdamThreads, 0);
+    c->adam_blocks = c->sms * std::max(aocc, 1);
+    c->shadow_blocks = c->sms * 2;
+    c->misc_blocks = c->sms * 4;
+
+    // exchange blob
+    Blob b{};
+    b.magic = kMagic;
+    b.token = process_token();
+    b.world_size = c->n;
+    b.rank = c->rank;
+    b.device = c->dev;
+    b.dtype = c->dtype;
+    b.layout_hash = c->layout_hash;
+    b.padded_numel = c->P_pad;
+    void* ptrs[5] = {grad, p, m, v, c->pad};
+    PFN_getAddressRange getRange = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CU(cudaGetDriverEntryPoint("cuMemGetAddressRange", (void**)&getRange, cudaEnableDefault, &q));
+    if (!getRange) return fail(c, CM_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    for (int k = 0; k < 5; ++k) {
+        CUdeviceptr base = 0;
+        size_t sz = 0;
+        if (getRange(&base, &sz, (CUdeviceptr)ptrs[k]) != CUDA_SUCCESS)
+            return fail(c, CM_ERR_ARG, "buffer %d is not a device allocation", k);
+        b.base[k] = (uint64_t)base;
+        b.offset[k] = (uint64_t)((char*)ptrs[k] - (char*)base);
+        b.raw[k] = (uint64_t)ptrs[k];
+        CU(cudaIpcGetMemHandle(&b.handle[k], (void*)base));
+    }
+    memcpy(blob_out, &b, sizeof b);
+    *blob_len = sizeof b;
+    c->registered = true;
+    return CM_OK;
+}
+
+static cm_status open_peer(cm_ctx* c, const Blob& b, int k, void** out) {
+    const uint64_t key = b.base[k] ^ (b.token * 0x9E3779B97F4A7C15ull);
+    for (auto& e : c->opened)
+        if (e.first == key) { *out = (char*)e.second + b.offset[k]; return CM_OK; }
+    void* ptr = nullptr;
+    CU(cudaIpcOpenMemHandle(&ptr, b.handle[k], cudaIpcMemLazyEnablePeerAccess));
+    c->opened.push_back({key, ptr});
+    *out = (char*)ptr + b.offset[k];
+    return CM_OK;
+}
+
+static cm_status create_or_attach_segment(cm_ctx* c);
+
+cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
+    if (!c) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->registered) return fail(c, CM_ERR_STATE, "cm_register_buckets first");
+    if (c->connected) return fail(c, CM_ERR_STATE, "already connected");
+    if (!blobs || blob_len != sizeof(Blob)) return fail(c, CM_ERR_ARG, "bad blobs");
+    CU(cudaSetDevice(c->dev));
+    std::vector<Blob> B(c->n);
+    memcpy(B.data(), blobs, sizeof(Blob) * c->n);
+    bool all_local = true, same_dev = true;
+    for (int k = 0; k < c->n; ++k) {
+        if (B[k].magic != kMagic || B[k].world_size != c->n || B[k].rank != k)
+            return fail(c, CM_ERR_CONFIG, "blob %d malformed or out of rank order", k);
+        if (B[k].layout_hash != c->layout_hash || B[k].padded_numel != c->P_pad || B[k].dtype != c->dtype)
+            return fail(c, CM_ERR_CONFIG, "rank %d registered a different layout", k);
+        if (B[k].token != process_token()) all_local = false;
+        if (B[k].device != c->dev) same_dev = false;
+    }
+    c->in_process = all_local;
+    // ranks that share one device and one process are "virtual ranks": the caller issues
+    // them on one stream in order, so no kernel ever waits for another and no barrier is
+    // needed (B200_PROFILING.md: never spin across launches on one GPU).
+    c->barriers = !(all_local && same_dev);
+    for (int k = 0; k < c->n; ++k) {
+        void* ptr[5];
+        if (k == c->rank) {
+            for (int j = 0; j < 5; ++j) ptr[j] = (void*)B[k].raw[j];
+        } else if (B[k].token == process_token()) {
+            if (B[k].device != c->dev) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(B[k].device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    return fail(c, CM_ERR_CONFIG, "no peer access %d->%d: %s", c->dev, B[k].device,
+                                cudaGetErrorString(e));
+                cudaGetLastError();
+            }
+            for (int j = 0; j < 5; ++j) ptr[j] = (void*)B[k].raw[j];
+        } else {
+            for (int j = 0; j < 5; ++j) {
+                cm_status s = open_peer(c, B[k], j, &ptr[j]);
+                if (s != CM_OK) return s;
+            }
+        }
+        c->peer_grad[k] = (char*)ptr[0];
+        c->peer_p[k] = (float*)ptr[1];
+        c->peer_m[k] = (float*)ptr[2];
+        c->peer_v[k] = (float*)ptr[3];
+        c->pads.p[k] = (uint32_t*)ptr[4];
+    }
+    if (!c->no_tap) {
+        cm_status s = create_or_attach_segment(c);
+        if (s != CM_OK) return s;
+    }
+    c->issued.assign(c->buckets.size(), 0);
+    c->issued_count = 0;
+    c->cur_iter = 0;
+    c->train_step = 0;
+    c->shadow_enq = 0;
+    c->connected = true;
+    return CM_OK;
+}
+
+static cm_status snapshot_state(cm_ctx* c, int half, cudaStream_t s) {
+    // shard r of this rank's p/m/v -> shadow half `half` (shard-local), one kernel
+    ShardCopyParams P{};
+    P.src[0] = c->p; P.src[1] = c->m; P.src[2] = c->v;
+    for (int a = 0; a < 3; ++a) P.dst[a][0] = c->st_dev[half][a];
+    P.buckets = c->d_buckets;
+    P.nb = (int)c->buckets.size();
+    P.n = c->n;
+    P.rank = c->rank;
+    P.dir = 0;
+    P.barriers = 0;
+    P.shard_nvec = c->shard_numel / 4;
+    int64_t want = (P.shard_nvec + 255) / 256;
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c->misc_blocks));
+    shard_copy_kernel<<<grid, 256, 0, s>>>(P);
+    c->launches++;
+    CHECK_LAUNCH();
+    return CM_OK;
+}
+
+static cm_status create_or_attach_segment(cm_ctx* c) {
+    char name[256];
+    snprintf(name, sizeof name, "/%s.r%d", c->shm_name.c_str(), c->rank);
+    const size_t nb = c->buckets.size();
+    SegHeader h{};
+    h.magic = kMagic;
+    h.version = kVersion;
+    h.world_size = c->n;
+    h.rank = c->rank;
+    h.dtype = c->dtype;
+    h.ring_depth = c->D;
+    h.n_buckets = (int32_t)nb;
+    h.shadow_place = c->shadow_place;
+    h.shard_numel = c->shard_numel;
+    h.layout_hash = c->layout_hash;
+    h.meta_off = kAlign;
+    h.flags_off = align_up(h.meta_off + sizeof(SlotMeta) * c->D, kAlign);
+    h.ring_off = align_up(h.flags_off + sizeof(uint64_t) * nb * c->D, kAlign);
+    h.state_off = align_up(h.ring_off + (size_t)c->D * c->shard_numel * c->es, kAlign);
+    const size_t state_bytes = c->shadow_place == CM_SHADOW_HOST ? 6 * (size_t)c->shard_numel * 4 : 0;
+    h.total = align_up(h.state_off + state_bytes, kAlign);
+
+    if (c->attach) {
+        c->shm_fd = shm_open(name, O_RDWR, 0600);
+        if (c->shm_fd < 0) return fail(c, CM_ERR_STATE, "attach: no shadow segment %s", name);
+        struct stat stt;
+        fstat(c->shm_fd, &stt);
+        if ((size_t)stt.st_size != h.total)
+            return fail(c, CM_ERR_STATE, "attach: segment %s has size %zu, layout needs %zu", name,
+                        (size_t)stt.st_size, (size_t)h.total);
+    } else {
+        shm_unlink(name);
+        c->shm_fd = shm_open(name, O_RDWR | O_CREAT | O_EXCL, 0600);
+        if (c->shm_fd < 0) return fail(c, CM_ERR_CONFIG, "shm_open(%s) failed: %s", name, strerror(errno));
+        if (ftruncate(c->shm_fd, (off_t)h.total) != 0)
+            return fail(c, CM_ERR_CONFIG, "ftruncate(%s, %zu) failed: %s", name, (size_t)h.total, strerror(errno));
+    }
+    c->seg_size = h.total;
+    void* mp = mmap(nullptr, c->seg_size, PROT_READ | PROT_WRITE, MAP_SHARED, c->shm_fd, 0);
+    if (mp == MAP_FAILED) return fail(c, CM_ERR_CONFIG, "mmap(%s) failed: %s", name, strerror(errno));
+    c->seg = (char*)mp;
+    c->hdr = (SegHeader*)c->seg;
+    if (c->attach) {
+        const SegHeader& e = *c->hdr;
+        if (e.magic != kMagic || e.version != kVersion || e.layout_hash != c->layout_hash ||
+            e.world_size != c->n || e.rank != c->rank || e.ring_depth != c->D || e.dtype != c->dtype ||
+            e.shard_numel != c->shard_numel || e.shadow_place != c->shadow_place || e.total != h.total)
+            return fail(c, CM_ERR_STATE, "attach: segment %s layout differs from this context", name);
+    } else {
+        memcpy(c->seg, &h, sizeof h);
+        c->hdr->shadow_step = -1;
+        c->hdr->half_step[0] = -1;
+        c->hdr->half_step[1] = -1;
+        for (int i = 0; i < c->D; ++i) slot_meta(c, i)->step_tag = -1;
+    }
+    CU(cudaHostRegister(c->seg, c->seg_size, cudaHostRegisterMapped | cudaHostRegisterPortable));
+    c->seg_registered = true;
+    CU(cudaHostGetDevicePointer((void**)&c->seg_dev, c->seg, 0));
+    if (c->shadow_place == CM_SHADOW_HOST) {
+        float* base = (float*)(c->seg + c->hdr->state_off);
+        for (int hf = 0; hf < 2; ++hf)
+            for (int a = 0; a < 3; ++a) {
+                c->st[hf][a] = base + ((size_t)hf * 3 + a) * c->shard_numel;
+                c->st_dev[hf][a] = to_dev(c, c->st[hf][a]);
+            }
+    } else {
+        if (c->attach) return fail(c, CM_ERR_STATE, "DEVICE-placed shadow cannot be attached after a restart");
+        CU(cudaMalloc(&c->state_dev_alloc, 6 * (size_t)c->shard_numel * 4));
+        for (int hf = 0; hf < 2; ++hf)
+            for (int a = 0; a < 3; ++a)
+                c->st[hf][a] = c->st_dev[hf][a] = c->state_dev_alloc + ((size_t)hf * 3 + a) * c->shard_numel;
+    }
+    if (!c->attach) {
+        // reading R19: the shadow starts as a copy of the step-0 training state
+        CU(cudaDeviceSynchronize());
+        cm_status s = snapshot_state(c, 0, 0);
+        if (s != CM_OK) return s;
+        CU(cudaDeviceSynchronize());
+        c->hdr->half_step[0] = 0;
+        c->hdr->shadow_step = 0;
+    }
+    return CM_OK;
+}
+
+cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* stream) {
+    if (!c) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
+    if (bucket < 0 || bucket >= (int32_t)c->buckets.size()) return fail(c, CM_ERR_ARG, "bucket %d out of range", bucket);
+    cudaStream_t s = S(stream);
+    if (t != c->cur_iter) {
+        if (t == c->cur_iter + 1 && c->issued_count == (int)c->buckets.size()) {
+            c->cur_iter = t;
+            std::fill(c->issued.begin(), c->issued.end(), 0);
+            c->issued_count = 0;
+        } else {
+            return fail(c, CM_ERR_STATE, "iteration %lld out of order (current %lld, %d/%zu buckets issued)",
+                        (long long)t, (long long)c->cur_iter, c->issued_count, c->buckets.size());
+        }
+    }
+    if (c->issued[bucket]) return fail(c, CM_ERR_STATE, "bucket %d of iteration %lld issued twice", bucket, (long long)t);
+    const int slot = (int)(t % c->D);
+    if (!c->no_tap && c->issued_count == 0 && t >= c->D) {
+        // lossless flow control: slot t mod D must have been consumed by the shadow's
+        // step t-D+1 (backpressure, never drop or overwrite)
+        if (c->shadow_enq < t - c->D + 1)
+            return fail(c, CM_ERR_STATE,
+                        "ring slot %d still holds iteration %lld: cm_shadow_apply(%lld) not enqueued",
+                        slot, (long long)(t - c->D), (long long)(t - c->D + 1));
+        CU(cudaStreamWaitEvent(s, c->ev_slot_free[slot], 0));
+    }
+    const BucketDev& B = c->buckets[bucket];
+    const int64_t shard = B.padded / c->n;
+    ArParams P{};
+    const int64_t byte_off = (B.off + (int64_t)c->rank * shard) * c->es;
+    for (int k = 0; k < c->n; ++k) P.buf[k] = c->peer_grad[k] + byte_off;
+    P.nvec = shard * c->es / 16;
+    P.pads = c->pads;
+    P.epoch = ++c->epoch;
+    P.rank = c->rank;
+    P.barriers = c->barriers ? 1 : 0;
+    P.ag = c->n > 1 ? 1 : 0;
+    const bool kernel_tap = !c->no_tap && !c->ce_tap;
+    P.tap = kernel_tap ? ring_slot_dev(c, slot) + B.shard_off * c->es : nullptr;
+    const int64_t want = (P.nvec + (int64_t)kArThreads * kArUnroll - 1) / ((int64_t)kArThreads * kArUnroll);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c->ar_blocks_max));
+    if (kernel_tap) {
+        P.done_ctr = c->d_done_ctr;
+        c->done_total += (unsigned long long)grid;
+        P.done_target = c->done_total;
+        P.tap_flag = to_dev(c, slot_flags(c, slot) + bucket);
+        P.tap_flag_value = (uint64_t)(t + 1);
+    }
+    if (c->dtype == CM_F32) launch_ar_t<F32Tag>(c->n, grid, s, P);
+    else launch_ar_t<BF16Tag>(c->n, grid, s, P);
+    c->launches++;
+    CHECK_LAUNCH();
+    if (!c->no_tap && c->ce_tap) {
+        // ablation: copy-engine tap of the reduced shard after the kernel (one extra HBM read)
+        CU(cudaMemcpyAsync(ring_slot_host(c, slot) + B.shard_off * c->es,
+                           c->peer_grad[c->rank] + byte_off, shard * c->es, cudaMemcpyDeviceToHost, s));
+        cm_status st = publish(c, (volatile int64_t*)(slot_flags(c, slot) + bucket), t + 1, s);
+        if (st != CM_OK) return st;
+    }
+    c->issued[bucket] = 1;
+    c->issued_count++;
+    if (!c->no_tap && c->issued_count == (int)c->buckets.size())
+        CU(cudaEventRecord(c->ev_tap_done[slot], s));
+    return CM_OK;
+}
+
+cm_status cm_apply_step(cm_ctx* c, int64_t step, const cm_adamw* hp, void* stream) {
+    if (!c || !hp) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
+    if (step != c->train_step + 1) return fail(c, CM_ERR_STATE, "step %lld follows %lld", (long long)step, (long long)c->train_step);
+    if (c->cur_iter != step - 1 || c->issued_count != (int)c->buckets.size())
+        return fail(c, CM_ERR_STATE, "step %lld before all buckets of iteration %lld were all-reduced (%d/%zu)",
+                    (long long)step, (long long)(step - 1), c->issued_count, c->buckets.size());
+    const AdamScalars a = make_scalars(c, step, *hp);
+    const int slot = (int)((step - 1) % c->D);
+    c->slot_sc[slot] = a;
+    c->slot_sc_step[slot] = step;
+    AdamParams P{};
+    P.g = c->grad;
+    P.p_in = c->p; P.m_in = c->m; P.v_in = c->v;
+    P.p_out = c->p; P.m_out = c->m; P.v_out = c->v;
+    P.n = c->P_pad;
+    P.s = a;
+    if (!c->no_tap) {
+        SlotMeta* sm = slot_meta(c, slot);
+        P.hp_rec = to_dev(c, sm->sc);
+        P.hp_tag = to_dev(c, &sm->step_tag);
+        P.step = step;
+    }
+    cm_status st = launch_adamw(c, P, c->adam_blocks, S(stream));
+    if (st != CM_OK) return st;
+    c->train_step = step;
+    return CM_OK;
+}
+
+static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars& a, cudaStream_t s) {
+    const int slot = (int)((step - 1) % c->D);
+    const int hin = (int)((step - 1) & 1), hout = (int)(step & 1);
+    cm_status st = publish(c, &c->hdr->half_step[hout], -1, s);   // half being rewritten
+    if (st != CM_OK) return st;
+    AdamParams P{};
+    P.g = ring_slot_dev(c, slot);
+    P.p_in = c->st_dev[hin][0]; P.m_in = c->st_dev[hin][1]; P.v_in = c->st_dev[hin][2];
+    P.p_out = c->st_dev[hout][0]; P.m_out = c->st_dev[hout][1]; P.v_out = c->st_dev[hout][2];
+    P.n = c->shard_numel;
+    P.s = a;
+    st = launch_adamw(c, P, c->shadow_blocks, s);
+    if (st != CM_OK) return st;
+    st = publish(c, &c->hdr->half_step[hout], step, s);
+    if (st != CM_OK) return st;
+    return publish(c, &c->hdr->shadow_step, step, s);
+}
+
+cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
+    if (!c) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
+    if (c->no_tap) return fail(c, CM_ERR_STATE, "context has no shadow (CM_FLAG_NO_TAP)");
+    if (step != c->shadow_enq + 1)
+        return fail(c, CM_ERR_STATE, "shadow step %lld after %lld: iteration gap", (long long)step, (long long)c->shadow_enq);
+    const int slot = (int)((step - 1) % c->D);
+    if (c->train_step < step || c->slot_sc_step[slot] != step)
+        return fail(c, CM_ERR_STATE, "shadow step %lld before cm_apply_step(%lld)", (long long)step, (long long)step);
+    cudaStream_t s = S(side_stream);
+    CU(cudaStreamWaitEvent(s, c->ev_tap_done[slot], 0));   // all taps of iteration step-1
+    cm_status st = shadow_step_enqueue(c, step, c->slot_sc[slot], s);
+    if (st != CM_OK) return st;
+    CU(cudaEventRecord(c->ev_slot_free[slot], s));          // release the ring slot
+    c->shadow_enq = step;
+    return CM_OK;
+}
+
+cm_status cm_gen_grads(cm_ctx* c, uint64_t seed, int64_t t, int32_t scale, void* stream) {
+    if (!c) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->registered) return fail(c, CM_ERR_STATE, "not registered");
+    const uint64_t K = [&] {
+        uint64_t x = seed ^ ((uint64_t)c->rank << 48) ^ (uint64_t)t;
+        uint64_t z = x + 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }();
+    const int64_t nvec = c->P_pad * c->es / 16;
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, c->misc_blocks));
+    if (c->dtype == CM_F32)
+        gen_grads_kernel<F32Tag><<<grid, 256, 0, S(stream)>>>(c->grad, nvec, c->d_buckets, (int)c->buckets.size(), K, scale);
+    else
+        gen_grads_kernel<BF16Tag><<<grid, 256, 0, S(stream)>>>(c->grad, nvec, c->d_buckets, (int)c->buckets.size(), K, scale);
+    c->launches++;
+    CHECK_LAUNCH();
+    return CM_OK;
+}
+
+cm_status cm_init_state(cm_ctx* c, uint64_t seed, void* stream) {
+    if (!c) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->registered) return fail(c, CM_ERR_STATE, "not registered");
+    const uint64_t K = [&] {
+        uint64_t x = seed ^ ((uint64_t)0xFFFF << 48) ^ 0ull;
+        uint64_t z = x + 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }();
+    const int64_t nvec = c->P_pad / 4;
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, c->misc_blocks));
+    init_state_kernel<<<grid, 256, 0, S(stream)>>>(c->p, c->m, c->v, nvec, c->d_buckets, (int)c->buckets.size(), K);
+    c->launches++;
+    CHECK_LAUNCH();
+    return CM_OK;
+}
+
+cm_status cm_verify(cm_ctx* c, int64_t* mismatch, void* stream) {
+    if (!c || !mismatch) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->connected || c->no_tap) return fail(c, CM_ERR_STATE, "no shadow to verify");
+    cudaStream_t s = S(stream);
+    CU(cudaStreamSynchronize(s));
+    CU(cudaDeviceSynchronize());
+    const int64_t step = c->hdr->shadow_step;
+    if (step < 0) return fail(c, CM_ERR_STATE, "shadow has no published step");
+    const int h = (int)(step & 1);
+    unsigned long long init = ~0ull;
+    CU(cudaMemcpy(c->d_bad, &init, sizeof init, cudaMemcpyHostToDevice));
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->shard_numel + 255) / 256, c->misc_blocks));
+    compare_kernel<<<grid, 256, 0, s>>>(c->st_dev[h][0], c->st_dev[h][1], c->st_dev[h][2], c->p, c->m, c->v,
+                                        c->d_buckets, (int)c->buckets.size(), c->n, c->rank, c->shard_numel,
+                                        c->d_bad);
+    c->launches++;
+    CHECK_LAUNCH();
+    unsigned long long bad = 0;
+    CU(cudaMemcpyAsync(&bad, c->d_bad, sizeof bad, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    *mismatch = bad == ~0ull ? -1 : (int64_t)bad;
+    if (bad != ~0ull) return fail(c, CM_ERR_INVARIANT, "shadow != train at flat index %llu (step %lld)", bad, (long long)step);
+    return CM_OK;
+}
+
+// ---------------------------------------------------------------- restore
+// Reading R21: every shard k can produce the steps
+// [lo_k, hi_k]: hi_k = its newest valid half plus the steps it can roll forward over
+// fully tapped ring slots (all bucket flags == step and the scalar record tagged step);
+// lo_k = its older half if that half is valid and holds hi-1, else its newest half.
+// I = min_k hi_k; restore fails (UNRECOVERABLE) if some lo_k > I.
+struct ShardReach {
+    int64_t newest = -1, older = -1, hi = -1, lo = -1;
+};
+
+static ShardReach reach_of(const SegHeader* h, const char* base, int D, int nb) {
+    ShardReach r;
+    int64_t a = h->half_step[0], b = h->half_step[1];
+    int64_t newest = std::max(a, b);
+    if (newest < 0) return r;
+    r.newest = newest;
+    int64_t other = (a == newest) ? b : a;
+    r.older = (other == newest - 1) ? other : -1;
+    int64_t hi = newest;
+    const SlotMeta* meta = (const SlotMeta*)(base + h->meta_off);
+    const volatile uint64_t* flags = (const volatile uint64_t*)(base + h->flags_off);
+    for (int64_t s = newest + 1; s <= newest + D; ++s) {
+        const int slot = (int)((s - 1) % D);
+        bool ok = meta[slot].step_tag == s;
+        for (int bkt = 0; ok && bkt < nb; ++bkt) ok = flags[(size_t)slot * nb + bkt] == (uint64_t)s;
+        if (!ok) break;
+        hi = s;
+    }
+    r.hi = hi;
+    r.lo = r.older >= 0 ? r.older : newest;
+    return r;
+}
+
+cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
+    if (!c || !restored) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->connected || c->no_tap) return fail(c, CM_ERR_STATE, "no shadow to restore from");
+    cudaStream_t s = S(stream);
+    CU(cudaDeviceSynchronize());
+    // consolidation over all shards (read-only views of the peers' segment headers)
+    int64_t I = INT64_MAX;
+    std::vector<ShardReach> R(c->n);
+    for (int k = 0; k < c->n; ++k) {
+        char name[256];
+        snprintf(name, sizeof name, "/%s.r%d", c->shm_name.c_str(), k);
+        const char* base = nullptr;
+        size_t len = 0;
+        int fd = -1;
+        if (k == c->rank) {
+            base = c->seg;
+        } else {
+            fd = shm_open(name, O_RDONLY, 0);
+            if (fd < 0) return fail(c, CM_ERR_UNRECOVERABLE, "shadow segment %s missing", name);
+            len = c->hdr->ring_off;   // header + meta + flags have the same layout on every rank
+            void* mp = mmap(nullptr, len, PROT_READ, MAP_SHARED, fd, 0);
+            close(fd);
+            if (mp == MAP_FAILED) return fail(c, CM_ERR_UNRECOVERABLE, "mmap %s failed", name);
+            base = (const char*)mp;
+        }
+        const SegHeader* h = (const SegHeader*)base;
+        bool ok = h->magic == kMagic && h->layout_hash == c->layout_hash && h->rank == k &&
+                  h->ring_depth == c->D;
+        if (ok) R[k] = reach_of(h, base, c->D, (int)c->buckets.size());
+        if (k != c->rank) munmap((void*)base, len);
+        if (!ok) return fail(c, CM_ERR_STATE, "shadow segment %s has a different layout", name);
+        if (R[k].hi < 0) return fail(c, CM_ERR_UNRECOVERABLE, "shard %d has no valid shadow state", k);
+        I = std::min(I, R[k].hi);
+    }
+    for (int k = 0; k < c->n; ++k)
+        if (R[k].lo > I)
+            return fail(c, CM_ERR_UNRECOVERABLE, "no common step: shard %d holds [%lld, %lld], target %lld", k,
+                        (long long)R[k].lo, (long long)R[k].hi, (long long)I);
+    // bring this shard to step I
+    const ShardReach& me = R[c->rank];
+    if (I == me.newest - 1) {
+        c->hdr->half_step[me.newest & 1] = -1;   // training will recompute that step
+        c->hdr->shadow_step = I;
+    } else {
+        for (int64_t st = me.newest + 1; st <= I; ++st) {   // roll forward over the ring
+            const int slot = (int)((st - 1) % c->D);
+            const SlotMeta* sm = slot_meta(c, slot);
+            AdamScalars a;
+            memcpy(&a, (const void*)sm->sc, sizeof a);
+            cm_status r = shadow_step_enqueue(c, st, a, s);
+            if (r != CM_OK) return r;
+        }
+    }
+    // host shadow shard -> all ranks' p/m/v (H2D + NVLink all-gather, one kernel)
+    ShardCopyParams P{};
+    const int h = (int)(I & 1);
+    for (int a = 0; a < 3; ++a) P.src[a] = c->st_dev[h][a];
+    for (int k = 0; k < c->n; ++k) {
+        P.dst[0][k] = c->peer_p[k];
+        P.dst[1][k] = c->peer_m[k];
+        P.dst[2][k] = c->peer_v[k];
+    }
+    P.buckets = c->d_buckets;
+    P.nb = (int)c->buckets.size();
+    P.n = c->n;
+    P.rank = c->rank;
+    P.dir = 1;
+    P.barriers = c->barriers ? 1 : 0;
+    P.shard_nvec = c->shard_numel / 4;
+    P.pads = c->pads;
+    P.epoch = ++c->epoch;
+    int64_t want = (P.shard_nvec + 255) / 256;
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, std::min(c->ar_blocks_max, kMaxBarrierBlocks)));
+    shard_copy_kernel<<<grid, 256, 0, s>>>(P);
+    c->launches++;
+    CHECK_LAUNCH();
+    CU(cudaStreamSynchronize(s));
+    c->cur_iter = I;
+    std::fill(c->issued.begin(), c->issued.end(), 0);
+    c->issued_count = 0;
+    c->train_step = I;
+    c->shadow_enq = I;
+    for (int i = 0; i < c->D; ++i) c->slot_sc_step[i] = -1;
+    *restored = I;
+    return CM_OK;
+}
+
+// ---------------------------------------------------------------- introspection
+cm_status cm_get_info(const cm_ctx* c, cm_info* o) {
+    if (!c || !o) return CM_ERR_ARG;
+    memset(o, 0, sizeof *o);
+    o->n_buckets = (int32_t)c->buckets.size();
+    o->world_size = c->n;
+    o->rank = c->rank;
+    o->ring_depth = c->D;
+    o->grad_dtype = c->dtype;
+    o->shadow_place = c->shadow_place;
+    o->peers_in_process = c->in_process ? 1 : 0;
+    o->padded_numel = c->P_pad;
+    o->shard_numel = c->shard_numel;
+    o->shadow_step = c->hdr ? c->hdr->shadow_step : -1;
+    o->launches = c->launches;
+    o->layout_hash = c->layout_hash;
+    return CM_OK;
+}
+
+cm_status cm_bucket_info(const cm_ctx* c, int32_t b, int64_t* off, int64_t* padded, int64_t* used) {
+    if (!c || b < 0 || b >= (int32_t)c->buckets.size()) return CM_ERR_ARG;
+    if (off) *off = c->buckets[b].off;
+    if (padded) *padded = c->buckets[b].padded;
+    if (used) *used = c->buckets[b].used;
+    return CM_OK;
+}
+
+cm_status cm_shadow_view(const cm_ctx* c, int32_t half, float** p, float** m, float** v) {
+    if (!c || half < 0 || half > 1 || !c->hdr) return CM_ERR_ARG;
+    if (p) *p = c->st[half][0];
+    if (m) *m = c->st[half][1];
+    if (v) *v = c->st[half][2];
+    return CM_OK;
+}
+
+cm_status cm_ring_view(const cm_ctx* c, int32_t slot, void** grads) {
+    if (!c || !c->hdr || slot < 0 || slot >= c->D || !grads) return CM_ERR_ARG;
+    *grads = c->seg + c->hdr->ring_off + (size_t)slot * c->shard_numel * c->es;
+    return CM_OK;
+}
+
+cm_status cm_unlink_shadow(const char* name, int32_t rank) {
+    if (!name) return CM_ERR_ARG;
+    char buf[256];
+    snprintf(buf, sizeof buf, "/%s.r%d", name, rank);
+    return shm_unlink(buf) == 0 ? CM_OK : CM_ERR_ARG;
+}
+
+cm_status cm_finalize(cm_ctx* c) {
+    if (!c) return CM_ERR_ARG;
+    if (c->registered || c->pad) cudaSetDevice(c->dev);
+    cudaDeviceSynchronize();
+    for (auto& e : c->opened) cudaIpcCloseMemHandle(e.second);
+    if (c->seg_registered) cudaHostUnregister(c->seg);
+    if (c->seg) munmap(c->seg, c->seg_size);
+    if (c->shm_fd >= 0) close(c->shm_fd);
+    if (c->state_dev_alloc) cudaFree(c->state_dev_alloc);
+    if (c->d_buckets) cudaFree(c->d_buckets);
+    if (c->pad) cudaFree(c->pad);
+    if (c->d_done_ctr) cudaFree(c->d_done_ctr);
+    if (c->d_bad) cudaFree(c->d_bad);
+    for (auto e : c->ev_tap_done) cudaEventDestroy(e);
+    for (auto e : c->ev_slot_free) cudaEventDestroy(e);
+    delete c;
+    return CM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,352 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element, bit-exact (north_star: "The GPU path must match the oracle bit-exactly").
+
+Ranks are virtual ranks on one GPU (n contexts in one process, issued on one stream): the
+kernels and data path are the ones the multi-GPU run uses; only the cross-GPU flag barrier
+is off (B200_PROFILING.md forbids kernels that wait on each other on one GPU).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2507_13522_b200 import cm, harness
+from paper_2507_13522_b200 import workloads as W
+from tests.gpu_util import assemble, bits, host_array, ring_flat, shadow_flat, t2np
+
+pytestmark = pytest.mark.gpu
+
+HP_O = dict(lr=W.HP["lr"], b1=W.HP["beta1"], b2=W.HP["beta2"], eps=W.HP["eps"], wd=W.HP["weight_decay"])
+_name_ctr = [0]
+
+
+def _name():
+    _name_ctr[0] += 1
+    return f"cmt{os.getpid()}_{_name_ctr[0]}"
+
+
+def make_group(numel, n, dtype=cm.CM_F32, cap=1 << 20, D=2, place=cm.CM_SHADOW_HOST, flags=0, seed=0):
+    name = _name()
+    g = harness.VirtualGroup(numel, n, 0, dtype, cap, name, D, place, flags, seed)
+    g._shm = name
+    return g
+
+
+def close(g):
+    g.sync()
+    g.finalize()
+    for r in range(g.n):
+        cm.unlink_shadow(g._shm, r)
+
+
+def oracle_for(numel, n, dtype, cap, seed=0):
+    plan = O.Plan(numel, cap, 4 if dtype == cm.CM_F32 else 2, n)
+    return plan, O.Run(plan, seed=seed, dtype=dtype, gscale=W.GRAD_SCALE, hp=HP_O)
+
+
+TABLES = {"c1": W.numels(W.c1()), "ragged": W.numels(W.c1_ragged()),
+          "mixed": [70000, 1, 3, 262145, 17, 5000, 300000, 2, 99999]}
+
+
+@pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+def test_inputs_match_oracle_generator(dtype, n):
+    numel = TABLES["ragged"]
+    g = make_group(numel, n, dtype)
+    plan = O.Plan(numel, 1 << 20, 4 if dtype == 0 else 2, n)
+    try:
+        g.gen(t=7)
+        g.sync()
+        for r in g.ranks:
+            np.testing.assert_array_equal(t2np(r.grad), O.gen_grads(plan, 0, r.rank, 7, dtype, W.GRAD_SCALE))
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(O.gen_p0(plan, 0)))
+            assert not r.m.any() and not r.v.any()
+    finally:
+        close(g)
+
+
+@pytest.mark.parametrize("table", ["c1", "ragged", "mixed"])
+@pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_iterations_bit_exact(table, dtype, n):
+    """Every element of R, the tap ring, train p/m/v and shadow p/m/v, every iteration."""
+    numel = TABLES[table]
+    iters = 10 if table == "c1" else 4
+    g = make_group(numel, n, dtype)
+    plan, ref = oracle_for(numel, n, dtype, 1 << 20)
+    try:
+        for t in range(iters):
+            g.step()
+            ref.step()
+            g.sync()
+            for r in g.ranks:
+                np.testing.assert_array_equal(bits(t2np(r.grad)), bits(ref.R), err_msg=f"R rank {r.rank} t {t}")
+            np.testing.assert_array_equal(bits(ring_flat(g, t % 2)), bits(ref.T), err_msg=f"tap t {t}")
+            for r in g.ranks:
+                for name, a, b in (("p", r.p, ref.p), ("m", r.m, ref.m), ("v", r.v, ref.v)):
+                    np.testing.assert_array_equal(bits(t2np(a)), bits(b), err_msg=f"{name} rank {r.rank} t {t}")
+            sp, sm, sv = shadow_flat(g, (t + 1) & 1)
+            for name, a, b in (("sp", sp, ref.sp), ("sm", sm, ref.sm), ("sv", sv, ref.sv)):
+                np.testing.assert_array_equal(bits(a), bits(b), err_msg=f"shadow {name} t {t}")
+            for r in g.ranks:
+                assert r.ctx.verify(g.stream) == -1
+                assert r.ctx.info().shadow_step == t + 1
+    finally:
+        close(g)
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_reduce_within_1e6_of_fp64(n):
+    numel = TABLES["c1"]
+    g = make_group(numel, n)
+    plan = O.Plan(numel, 1 << 20, 4, n)
+    try:
+        g.gen(t=0)
+        g.allreduce(t=0)
+        g.sync()
+        R = t2np(g.ranks[0].grad).astype(np.float64)
+        G = np.stack([O.gen_grads(plan, 0, r, 0, O.F32) for r in range(n)]).astype(np.float64)
+        err = np.abs(R - G.sum(0))
+        assert np.all(err <= 1e-6 * np.abs(G).sum(0))
+    finally:
+        close(g)
+
+
+def test_device_shadow_placement_bit_exact():
+    numel = TABLES["ragged"]
+    g = make_group(numel, 2, place=cm.CM_SHADOW_DEVICE)
+    plan, ref = oracle_for(numel, 2, cm.CM_F32, 1 << 20)
+    try:
+        for t in range(5):
+            g.step()
+            ref.step()
+            g.sync()
+            for r in g.ranks:
+                assert r.ctx.verify(g.stream) == -1
+            np.testing.assert_array_equal(bits(t2np(g.ranks[1].p)), bits(ref.p))
+    finally:
+        close(g)
+
+
+def test_copy_engine_tap_ablation_bit_exact():
+    numel = TABLES["ragged"]
+    g = make_group(numel, 4, flags=cm.CM_FLAG_TAP_COPYENGINE)
+    plan, ref = oracle_for(numel, 4, cm.CM_F32, 1 << 20)
+    try:
+        for t in range(3):
+            g.step()
+            ref.step()
+            g.sync()
+            np.testing.assert_array_equal(bits(ring_flat(g, t % 2)), bits(ref.T))
+            for r in g.ranks:
+                assert r.ctx.verify(g.stream) == -1
+    finally:
+        close(g)
+
+
+def test_no_tap_mode_matches_train_state():
+    numel = TABLES["c1"]
+    g = make_group(numel, 2, flags=cm.CM_FLAG_NO_TAP)
+    plan, ref = oracle_for(numel, 2, cm.CM_F32, 1 << 20)
+    try:
+        for t in range(3):
+            g.step()
+            ref.step()
+        g.sync()
+        np.testing.assert_array_equal(bits(t2np(g.ranks[0].p)), bits(ref.p))
+        with pytest.raises(cm.CMError):
+            g.ranks[0].ctx.shadow_apply(4, g.side)
+    finally:
+        close(g)
+
+
+def test_tap_exactly_once_covers_every_element():
+    """Poison the ring; after one iteration every element of every rank's slot was written
+    once with R (sum over ranks of tapped elements = padded elements, S)."""
+    numel = TABLES["ragged"]
+    n = 4
+    g = make_group(numel, n)
+    plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
+    try:
+        info = g.ranks[0].ctx.info()
+        for r in g.ranks:
+            ptr = r.ctx.ring_view(0)
+            import ctypes as C
+            C.memset(ptr, 0x7F, info.shard_numel * 4)   # 0x7F7F7F7F: finite poison never produced
+        g.step()
+        ref.step()
+        g.sync()
+        flat = ring_flat(g, 0)
+        assert not np.any(flat.view(np.uint32) == 0x7F7F7F7F)
+        np.testing.assert_array_equal(flat.view(np.uint32), ref.T.view(np.uint32))
+        assert n * info.shard_numel == plan.total
+    finally:
+        close(g)
+
+
+def test_flow_control_refuses_to_overwrite_unconsumed_slot():
+    numel = TABLES["c1"]
+    g = make_group(numel, 2, D=2)
+    try:
+        g.step(shadow=False)          # iteration 0 -> slot 0, not consumed
+        g.step(shadow=False)          # iteration 1 -> slot 1
+        g.gen()
+        with pytest.raises(cm.CMError) as e:
+            g.allreduce()             # iteration 2 would overwrite slot 0
+        assert e.value.status == cm.CM_ERR_STATE
+        g.shadow(step=1)
+        for r in g.ranks:             # slot 0 released: the same call now succeeds
+            pass
+        g.allreduce()
+        g.apply()
+        g.t += 1
+        g.shadow(step=2)
+        g.shadow(step=3)
+        g.sync()
+        for r in g.ranks:
+            assert r.ctx.verify(g.stream) == -1
+    finally:
+        close(g)
+
+
+def test_backpressure_with_slow_shadow_is_lossless():
+    """The shadow stream is throttled (sleep kernels): training blocks on the ring, never
+    overwrites, and the shadow stays bit-identical."""
+    numel = TABLES["ragged"]
+    g = make_group(numel, 2, D=2)
+    plan, ref = oracle_for(numel, 2, cm.CM_F32, 1 << 20)
+    try:
+        for t in range(8):
+            with torch.cuda.stream(g.side):
+                torch.cuda._sleep(20_000_000)      # ~10 ms at 2 GHz before each shadow step
+            g.step()
+            ref.step()
+        g.sync()
+        np.testing.assert_array_equal(bits(t2np(g.ranks[0].p)), bits(ref.p))
+        sp, sm, sv = shadow_flat(g, 8 & 1)
+        np.testing.assert_array_equal(bits(sp), bits(ref.sp))
+        np.testing.assert_array_equal(bits(sv), bits(ref.sv))
+    finally:
+        close(g)
+
+
+def test_state_errors():
+    numel = TABLES["c1"]
+    g = make_group(numel, 2)
+    try:
+        c = g.ranks[0].ctx
+        with pytest.raises(cm.CMError) as e:
+            c.apply_step(1, stream=g.stream)            # before any all-reduce
+        assert e.value.status == cm.CM_ERR_STATE
+        with pytest.raises(cm.CMError) as e:
+            c.allreduce_multicast(0, 5, g.stream)       # iteration gap
+        assert e.value.status == cm.CM_ERR_STATE
+        with pytest.raises(cm.CMError) as e:
+            c.allreduce_multicast(99, 0, g.stream)      # bucket out of range
+        assert e.value.status == cm.CM_ERR_ARG
+        c.allreduce_multicast(0, 0, g.stream)
+        with pytest.raises(cm.CMError) as e:
+            c.allreduce_multicast(0, 0, g.stream)       # same bucket twice
+        assert e.value.status == cm.CM_ERR_STATE
+        with pytest.raises(cm.CMError) as e:
+            c.apply_step(1, stream=g.stream)            # partial iteration: no partial update
+        assert e.value.status == cm.CM_ERR_STATE
+        with pytest.raises(cm.CMError) as e:
+            c.shadow_apply(1, g.side)                   # before cm_apply_step(1)
+        assert e.value.status == cm.CM_ERR_STATE
+    finally:
+        close(g)
+
+
+@pytest.mark.parametrize("lag", [0, 1])
+@pytest.mark.parametrize("n", [2, 4])
+def test_soft_restore_continues_bit_exact(n, lag):
+    """Kill (poison the training state) at iteration k, restore from the shadow, continue:
+    identical to the uninterrupted run (PAPER.md:601 methodology)."""
+    numel = TABLES["ragged"]
+    k, more = 5, 5
+    g = make_group(numel, n, D=2)
+    plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
+    try:
+        for t in range(k):
+            g.step(shadow=(t < k - lag))              # lag=1: the shadow misses the last step
+        g.sync()
+        for r in g.ranks:
+            r.p.fill_(float("nan")); r.m.fill_(float("nan")); r.v.fill_(float("nan"))
+        torch.cuda.synchronize()
+        steps = [r.ctx.restore(g.stream) for r in g.ranks]
+        assert steps == [k] * n                       # roll-forward recovers the lagging step
+        for _ in range(k):
+            ref.step()
+        for r in g.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            np.testing.assert_array_equal(bits(t2np(r.m)), bits(ref.m))
+            np.testing.assert_array_equal(bits(t2np(r.v)), bits(ref.v))
+        g.t = k
+        for _ in range(more):
+            g.step()
+            ref.step()
+        g.sync()
+        for r in g.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            assert r.ctx.verify(g.stream) == -1
+    finally:
+        close(g)
+
+
+@pytest.mark.parametrize("n", [1, 8])
+def test_gpt2_full_size_sampled(n):
+    """GPT-2 small at full size (124,439,808 params, 17 buckets): 3 iterations, sampled
+    elements vs the oracle's per-element trajectories (PAPER.md:306-308 independence)."""
+    numel = W.numels(W.gpt2_small())
+    g = make_group(numel, n, cap=W.CAP_BYTES)
+    try:
+        steps = 3
+        for _ in range(steps):
+            g.step()
+        g.sync()
+        plan = O.Plan(numel, W.CAP_BYTES, 4, n)
+        rng = np.random.default_rng(0)
+        idx = rng.choice(plan.total, 1 << 15, replace=False)
+        edges = np.concatenate([plan.bucket_off, plan.bucket_off + plan.bucket_padded - 1])
+        idx = np.unique(np.concatenate([idx, edges])).astype(np.int64)
+        used = plan.used_mask()[idx]
+        p, m, v, R = O.run_sample(0, n, O.F32, W.GRAD_SCALE, steps, idx, used, **HP_O)
+        for r in g.ranks:
+            ti = torch.from_numpy(idx).to(r.p.device)
+            np.testing.assert_array_equal(bits(r.p[ti].cpu().numpy()), bits(p))
+            np.testing.assert_array_equal(bits(r.m[ti].cpu().numpy()), bits(m))
+            np.testing.assert_array_equal(bits(r.v[ti].cpu().numpy()), bits(v))
+            np.testing.assert_array_equal(bits(r.grad[ti].cpu().numpy()), bits(R))
+            assert r.ctx.verify(g.stream) == -1
+    finally:
+        close(g)
+
+
+def test_llama_shaped_bf16_sampled():
+    """Llama-3-8B-shaped layers (first 2 decoder layers + norms, bf16 grads, 25 MiB cap,
+    dedicated buckets for the big matrices) at n=8, sampled vs the oracle."""
+    t = W.llama3_8b()
+    numel = [x for _, x in t[1:19]] + [4096]       # 2 layers + final norm (no 1 GB embeddings)
+    n = 8
+    g = make_group(numel, n, dtype=cm.CM_BF16, cap=W.CAP_BYTES)
+    try:
+        for _ in range(2):
+            g.step()
+        g.sync()
+        plan = O.Plan(numel, W.CAP_BYTES, 2, n)
+        idx = np.unique(np.random.default_rng(1).choice(plan.total, 1 << 15, replace=False)).astype(np.int64)
+        used = plan.used_mask()[idx]
+        p, m, v, R = O.run_sample(0, n, O.BF16, W.GRAD_SCALE, 2, idx, used, **HP_O)
+        r = g.ranks[3]
+        ti = torch.from_numpy(idx).to(r.p.device)
+        np.testing.assert_array_equal(bits(r.p[ti].cpu().numpy()), bits(p))
+        np.testing.assert_array_equal(bits(r.v[ti].cpu().numpy()), bits(v))
+        Rg = (t2np(r.grad[ti]).astype(np.uint32) << 16).view(np.float32)
+        np.testing.assert_array_equal(bits(Rg), bits(R))
+        for rr in g.ranks:
+            assert rr.ctx.verify(g.stream) == -1
+    finally:
+        close(g)
