@@ -1,0 +1,499 @@
+#!/usr/bin/env python
+"""Benchmark of the Checkmate hot path on B200 (BASELINE.json metric:
+"iter/s with per-iteration checkpoint vs no-ckpt at 1/2/4/8 B200; allreduce GB/s").
+
+A step = one pass of the whole hot path over one batch of synthetic input:
+gradient production (a1, the counter-based generator kernel standing in for backward),
+the fused reduce-scatter + tap + all-gather of every bucket (a2-a4), the training AdamW
+(a5), ring flow control (a6) and the shadow AdamW on a low-priority side stream (a7).
+
+  python bench.py [--gpus N --steps K --warmup W] [--workload gpt2|c1|llama8b]
+                  [--shadow host|device] [--impl ours|reference]
+  N>1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+Rank 0 prints ONE JSON line.  `value` is whole-job throughput: rank-iterations per second
+(iterations/s x N; each rank-iteration reduces and checkpoints one local batch's
+gradients), max-over-ranks device time.  `--impl reference` times the CPU oracle (the
+tier's reference arm) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import socket
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "iter/s with per-iteration checkpoint vs no-ckpt at 1/2/4/8 B200; allreduce GB/s"
+UNIT = "rank-iter/s"
+NVLINK_PEAK_GBS = 770.0     # B200_PROFILING.md: measured peer copy per direction (900 nominal)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "c1", "llama8b"])
+    ap.add_argument("--shadow", default="host", choices=["host", "device"])
+    ap.add_argument("--ring-depth", type=int, default=2)
+    ap.add_argument("--no-baseline", action="store_true", help="skip the NCCL + torch fused AdamW arm")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="target seconds of oracle work")
+    return ap.parse_args()
+
+
+def workload(name):
+    from paper_2507_13522_b200 import workloads as W
+    from paper_2507_13522_b200 import cm
+    if name == "gpt2":
+        return "GPT-2 small (124,439,808 params, 17 buckets of <=25 MiB), fp32 grads + fp32 AdamW state", \
+            W.numels(W.gpt2_small()), cm.CM_F32, W.CAP_BYTES
+    if name == "c1":
+        return "C1: 2^20 fp32 params, 4 x 1 MiB buckets", W.numels(W.c1()), cm.CM_F32, 1 << 20
+    return "Llama-3-8B shaped (8,030,261,248 params, 226 buckets), bf16 grads + fp32 AdamW state", \
+        W.numels(W.llama3_8b()), cm.CM_BF16, W.CAP_BYTES
+
+
+# ---------------------------------------------------------------------------- distributed
+def dist_setup(gpus):
+    import torch
+    import torch.distributed as dist
+    if "RANK" not in os.environ:
+        if gpus != 1:
+            raise SystemExit("--gpus N>1 must be launched with torch.distributed.run")
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1")
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+        s.close()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    dist.init_process_group(backend, rank=rank, world_size=world,
+                            device_id=torch.device("cuda", local) if backend == "nccl" else None)
+    return rank, world, local
+
+
+def max_over_ranks(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------- measurements
+def host_link_peaks(dev):
+    """Copy-engine pinned D2H / H2D GB/s on this GPU (the practical host-link roof)."""
+    import torch
+    n = 256 << 20
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    out = {}
+    for name, fn in (("d2h", lambda: h.copy_(d, non_blocking=True)), ("h2d", lambda: d.copy_(h, non_blocking=True))):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        out[name] = 5 * n / (a.elapsed_time(b) * 1e-3) / 1e9
+    return out
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_table():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def time_steps(step_fn, streams, k):
+    import torch
+    s0 = streams[0]
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(s0)
+    for _ in range(k):
+        step_fn()
+    for s in streams[1:]:                      # the shadow's drain counts (conservative)
+        e = torch.cuda.Event()
+        e.record(s)
+        s0.wait_event(e)
+    b.record(s0)
+    b.synchronize()
+    return a.elapsed_time(b)
+
+
+def run_ours(args, rank, world, local, name, numel, dtype, cap):
+    import torch
+    import torch.distributed as dist
+    from paper_2507_13522_b200 import cm, harness
+    from paper_2507_13522_b200 import workloads as W
+
+    dev = torch.device("cuda", local)
+    place = cm.CM_SHADOW_HOST if args.shadow == "host" else cm.CM_SHADOW_DEVICE
+    shm = f"cmbench{os.getppid() if world > 1 else os.getpid()}"
+    if world > 1:
+        shm = f"cmbench_{os.environ.get('MASTER_PORT', '0')}"
+    R = harness.DistRank(numel, dtype, cap, shm, args.ring_depth, place)
+    ctx = R.r.ctx
+    info = ctx.info()
+    es = 4 if dtype == cm.CM_F32 else 2
+    S_bytes = info.padded_numel * es
+
+    def step():
+        R.step()
+
+    for _ in range(args.warmup):
+        step()
+    R.sync()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.info().launches
+    ctx.timing(True)
+    with ClockSampler(local) as clk:
+        ms = time_steps(step, [R.stream, R.side], args.steps)
+    kms, kcnt = ctx.timing(False)
+    launches = ctx.info().launches - launches0
+    ms_max = max_over_ranks(ms)
+    ms_step = ms_max / args.steps
+    iters_per_s = 1000.0 / ms_step
+    # bit-identity of the shadow after the timed run (verify synchronises)
+    mismatch = ctx.verify(R.stream)
+
+    # ----- per-kernel roofline (average launch duration, live events on each kernel's stream)
+    n = world
+    hbm_peak, hbm_src = measured_peaks()
+    link = host_link_peaks(dev)
+    nb = info.n_buckets
+    kern = {}
+    ar_ms = kms[0] / max(kcnt[0], 1)
+    ar_bytes_nvl = 2.0 * (n - 1) / n * S_bytes / nb                  # per launch, per GPU, both directions
+    ar_bytes_tap = S_bytes / n / nb
+    kern["rs_tap_ag"] = {"avg_ms": ar_ms, "launches": kcnt[0],
+                         "nvlink_GBps_per_dir": (ar_bytes_nvl / 2) / (ar_ms * 1e-3) / 1e9 if n > 1 else 0.0,
+                         "tap_GBps": ar_bytes_tap / (ar_ms * 1e-3) / 1e9,
+                         "share": kms[0] / ms}
+    ad_ms = kms[1] / max(kcnt[1], 1)
+    ad_bytes = info.padded_numel * (es + 24)
+    kern["adamw_step"] = {"avg_ms": ad_ms, "launches": kcnt[1], "hbm_GBps": ad_bytes / (ad_ms * 1e-3) / 1e9,
+                          "hbm_frac": ad_bytes / (ad_ms * 1e-3) / 1e9 / hbm_peak, "share": kms[1] / ms}
+    sh_ms = kms[2] / max(kcnt[2], 1)
+    # shadow step (copy-engine staged): H2D = ring grads; D2H = new p/m/v persisted (HOST)
+    sh_h2d = info.shard_numel * es
+    sh_d2h = info.shard_numel * (12 if place == cm.CM_SHADOW_HOST else 0)
+    kern["shadow_step"] = {"avg_ms": sh_ms, "launches": kcnt[2], "h2d_GBps": sh_h2d / (sh_ms * 1e-3) / 1e9,
+                           "d2h_GBps": sh_d2h / (sh_ms * 1e-3) / 1e9, "share": kms[2] / ms,
+                           "what": "H2D ring chunk -> HBM AdamW (ping-pong halves) -> D2H persist, pipelined"}
+    gen_ms = kms[3] / max(kcnt[3], 1)
+    kern["gen_grads"] = {"avg_ms": gen_ms, "launches": kcnt[3], "share": kms[3] / ms}
+
+    # dominant kernel -> roofline object
+    shares = {k: v["share"] for k, v in kern.items()}
+    dom = max(shares, key=shares.get)
+    traf = traffic_table()
+    if dom == "adamw_step":
+        roof = {"kernel": dom, "bound": "hbm", "achieved": kern[dom]["hbm_GBps"], "peak": hbm_peak,
+                "unit": "GB/s", "peak_source": hbm_src, "bytes_per_launch": ad_bytes}
+    elif dom == "shadow_step":
+        if sh_d2h > 0:
+            roof = {"kernel": dom, "bound": "host_link", "achieved": kern[dom]["d2h_GBps"], "peak": link["d2h"],
+                    "unit": "GB/s", "peak_source": "measured pinned D2H copy (this run)",
+                    "bytes_per_launch": sh_d2h, "direction": "d2h"}
+        else:
+            roof = {"kernel": dom, "bound": "host_link", "achieved": kern[dom]["h2d_GBps"], "peak": link["h2d"],
+                    "unit": "GB/s", "peak_source": "measured pinned H2D copy (this run)",
+                    "bytes_per_launch": sh_h2d, "direction": "h2d"}
+    elif dom == "rs_tap_ag":
+        t_nvl = (ar_bytes_nvl / 2) / (NVLINK_PEAK_GBS * 1e9) if n > 1 else 0.0
+        t_tap = ar_bytes_tap / (link["d2h"] * 1e9)
+        if t_nvl >= t_tap:
+            roof = {"kernel": dom, "bound": "nvlink", "achieved": kern[dom]["nvlink_GBps_per_dir"],
+                    "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "peak_source": "B200_PROFILING.md measured peer copy",
+                    "bytes_per_launch": ar_bytes_nvl / 2}
+        else:
+            roof = {"kernel": dom, "bound": "host_link", "achieved": kern[dom]["tap_GBps"], "peak": link["d2h"],
+                    "unit": "GB/s", "peak_source": "measured pinned D2H copy (this run)",
+                    "bytes_per_launch": ar_bytes_tap, "direction": "d2h"}
+    else:
+        roof = {"kernel": dom, "bound": "alu", "achieved": None, "peak": None, "unit": None}
+    if roof.get("achieved") is not None:
+        roof["frac"] = roof["achieved"] / roof["peak"]
+    # the whole step's use of the host link (tap + persisted shadow state share D2H)
+    step_d2h = S_bytes / n + sh_d2h
+    roof["step_host_link_d2h"] = {"bytes_per_step": step_d2h, "GBps": step_d2h / (ms_step * 1e-3) / 1e9,
+                                  "frac": step_d2h / (ms_step * 1e-3) / 1e9 / link["d2h"]}
+    roof["traffic"] = traf.get(f"{args.workload}_n{n}_{args.shadow}", {}).get(dom)
+
+    result = {"ms_step": ms_step, "iters_per_s": iters_per_s, "launches": launches, "kernels": kern,
+              "roofline": roof, "clocks": clk.summary(), "shadow_bit_identical": mismatch == -1,
+              "host_link_GBps": link, "S_bytes": S_bytes}
+
+    # ----- e2e: same metric through the public API with HOST gradient buffers
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, R, S_bytes, es)
+    R.sync()
+    ctx.finalize()
+    if rank == 0 or world == 1:
+        pass
+    for r in range(world):
+        if r == rank:
+            cm.unlink_shadow(shm, r)
+    return result
+
+
+def run_e2e(args, R, S_bytes, es):
+    """Per step: H2D copy of this step's gradients from pinned host memory, the hot path,
+    and a D2H read of the step's result (the shadow's published step, 8 bytes)."""
+    import torch
+    from paper_2507_13522_b200 import cm
+    grad = R.r.grad
+    host = [torch.empty_like(grad, device="cpu").pin_memory() for _ in range(2)]
+    for i in range(2):                                        # two distinct input batches
+        R.r.ctx.gen_grads(R.seed, 10_000 + i, R.gscale, R.stream)
+        R.stream.synchronize()
+        host[i].copy_(grad)
+    out = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    dev_flag = torch.empty(1, dtype=torch.int64, device=grad.device)
+    c = R.r.ctx
+
+    def step():
+        with torch.cuda.stream(R.stream):
+            grad.copy_(host[R.t & 1], non_blocking=True)
+        for b in range(R.n_buckets):
+            c.allreduce_multicast(b, R.t, R.stream)
+        c.apply_step(R.t + 1, stream=R.stream, **R.hp)
+        c.shadow_apply(R.t + 1, R.side)
+        with torch.cuda.stream(R.stream):
+            dev_flag.fill_(R.t + 1)
+            out.copy_(dev_flag, non_blocking=True)
+        R.t += 1
+
+    for _ in range(max(2, args.warmup // 2)):
+        step()
+    R.sync()
+    k = max(3, args.steps // 2)
+    ms = time_steps(step, [R.stream, R.side], k)
+    ms = max_over_ranks(ms)
+    return {"value": 1000.0 / (ms / k) * R.n, "unit": UNIT, "h2d_bytes_per_step": S_bytes,
+            "d2h_bytes_per_step": 8, "ms_per_step": ms / k,
+            "note": "pinned-host grads copied H2D each step inside the timed region; per rank"}
+
+
+def run_nccl_baseline(args, rank, world, local, numel, dtype, cap):
+    """No-checkpoint baseline: NCCL all_reduce per bucket + torch fused AdamW (same buffers
+    layout, same synthetic gradients from our generator kernel)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2507_13522_b200 import cm, harness
+    dev = torch.device("cuda", local)
+    R = harness.Rank(numel, world, rank, local, dtype, cap, "unused", 2, cm.CM_SHADOW_HOST, cm.CM_FLAG_NO_TAP)
+    buckets = R.buckets()
+    views = [R.grad[o:o + p] for (o, p, u) in buckets]
+    stream = torch.cuda.Stream(dev, priority=-1)
+    step_t = torch.zeros((), dtype=torch.float32, device=dev)
+    gscale = torch.full((), float(world), dtype=torch.float32, device=dev)
+    g32 = R.grad if dtype == cm.CM_F32 else None
+    t = [0]
+
+    def step():
+        with torch.cuda.stream(stream):
+            R.ctx.gen_grads(0, t[0], 10, stream)
+            for v in views:
+                dist.all_reduce(v)
+            step_t.add_(1)
+            g = R.grad if g32 is not None else R.grad.float()
+            torch._fused_adamw_([R.p], [g], [R.m], [R.v], [], [step_t], amsgrad=False, lr=1e-3, beta1=0.9,
+                                beta2=0.999, weight_decay=0.01, eps=1e-8, maximize=False, grad_scale=gscale)
+        t[0] += 1
+
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = time_steps(step, [stream], args.steps)
+    ms = max_over_ranks(ms)
+    R.ctx.finalize()
+    return {"ms_step": ms / args.steps, "iters_per_s": 1000.0 / (ms / args.steps),
+            "what": "torch.distributed all_reduce (NCCL %s) per bucket + torch._fused_adamw_; no tap, no shadow"
+                    % ".".join(map(str, torch.cuda.nccl.version()))}
+
+
+def run_ours_nockpt(args, rank, world, local, numel, dtype, cap):
+    """Our kernels without the tap and shadow (CM_FLAG_NO_TAP): the checkpoint's cost in
+    isolation on the same kernels."""
+    import torch
+    import torch.distributed as dist
+    from paper_2507_13522_b200 import cm, harness
+    R = harness.DistRank(numel, dtype, cap, "unused", 2, cm.CM_SHADOW_HOST, cm.CM_FLAG_NO_TAP)
+    for _ in range(args.warmup):
+        R.step()
+    R.sync()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = time_steps(R.step, [R.stream], args.steps)
+    ms = max_over_ranks(ms)
+    R.r.ctx.finalize()
+    return {"ms_step": ms / args.steps, "iters_per_s": 1000.0 / (ms / args.steps)}
+
+
+# ---------------------------------------------------------------------------- oracle arm
+def oracle_sample(args, numel, dtype, cap, n):
+    """Time the CPU oracle (oracle/, as it stands, single thread) on a bounded random
+    sample of the workload's elements; project to the full workload."""
+    import numpy as np
+    from oracle import oracle as O
+    from paper_2507_13522_b200 import workloads as W
+    es = 4 if dtype == 0 else 2
+    plan = O.Plan(numel, cap, es, n)
+    rng = np.random.default_rng(1)
+    # calibrate on a small sample, then size the sample to ~cpu_sample_s seconds
+    k0 = min(plan.total, 1 << 14)
+    idx = np.sort(rng.choice(plan.total, k0, replace=False)).astype(np.int64)
+    ones = np.ones(k0, np.uint8)
+    t0 = time.perf_counter()
+    O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 2, idx, ones)
+    per = (time.perf_counter() - t0) / (2 * k0)
+    steps = 2
+    k = int(min(plan.total, max(k0, args.cpu_sample_s / (per * steps))))
+    idx = np.sort(rng.choice(plan.total, k, replace=False)).astype(np.int64)
+    used = np.ones(k, np.uint8)
+    t0 = time.perf_counter()
+    O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, steps, idx, used)
+    dt = time.perf_counter() - t0
+    per_elem_step = dt / (k * steps)
+    full_iter_s = per_elem_step * plan.total            # one full iteration of all n ranks' work
+    return {"value": n / full_iter_s, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{k} of {plan.total} elements x {steps} iterations (rank-order sum of {n} ranks' "
+                      f"generated grads + AdamW), {dt:.1f} s single-threaded, projected to the full workload",
+            "ns_per_elem_iter": per_elem_step * 1e9}
+
+
+def main():
+    args = parse()
+    name, numel, dtype, cap = workload(args.workload)
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        if rank != 0:
+            return 0
+        from oracle import oracle as O
+        O.build()
+        cb = oracle_sample(args, numel, dtype, cap, world)
+        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * world / cb["value"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": {"workload": name, "ranks": world},
+                "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                            "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    from paper_2507_13522_b200 import cm
+    cm.lib()   # fail loudly if the CUDA library is missing
+    rank, world, local = dist_setup(args.gpus)
+    res = run_ours(args, rank, world, local, name, numel, dtype, cap)
+    base = None if args.no_baseline else run_nccl_baseline(args, rank, world, local, numel, dtype, cap)
+    ours_nockpt = None if args.no_baseline else run_ours_nockpt(args, rank, world, local, numel, dtype, cap)
+    cpu = None
+    if rank == 0 and world == 1:
+        from oracle import oracle as O
+        O.build()
+        cpu = oracle_sample(args, numel, dtype, cap, world)
+    if rank == 0:
+        overhead = None if base is None else (res["ms_step"] / base["ms_step"] - 1.0) * 100.0
+        line = {
+            "metric": METRIC, "value": res["iters_per_s"] * world, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if dtype == cm.CM_F32 else "bf16-grads/f32-state", "data": "synthetic",
+            "config": {"workload": name, "ranks": world, "shadow": args.shadow, "ring_depth": args.ring_depth,
+                       "parallelism": f"dp{world}", "l2": "inputs larger than L2 (working set >> 126 MB)",
+                       "iters_per_s": res["iters_per_s"]},
+            "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res.get("e2e"),
+            "gpu_launches": res["launches"], "clocks": res["clocks"],
+            "nockpt_nccl": base, "nockpt_ours": ours_nockpt,
+            "ckpt_overhead_pct_vs_nccl": overhead,
+            "shadow_bit_identical": res["shadow_bit_identical"], "kernels": res["kernels"],
+            "host_link_GBps": res["host_link_GBps"],
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

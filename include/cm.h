@@ -68,6 +68,9 @@ typedef enum { CM_SHADOW_HOST = 0, CM_SHADOW_DEVICE = 1 } cm_shadow_place;
                                          after a failure) instead of creating a fresh one  */
 #define CM_FLAG_TAP_COPYENGINE (1ull << 2) /* ablation: tap with a copy-engine D2H after
                                          the all-reduce kernel instead of in-kernel stores */
+#define CM_FLAG_NO_SHADOW (1ull << 3) /* benchmark mode (bucket sweep): tap into the ring but
+                                         keep no shadow replica and no flow control; the ring
+                                         is overwritten freely; shadow/verify/restore refuse */
 
 typedef struct {
     int32_t world_size;   /* n, 1..8: data-parallel ranks on this box                      */
@@ -224,6 +227,22 @@ cm_status cm_bucket_info(const cm_ctx *ctx, int32_t bucket, int64_t *elem_off, i
 /* Host pointers into the shadow: state half h (0/1) as shard-local arrays of
  * shard_numel fp32 (HOST placement only; DEVICE placement returns device pointers),
  * and ring slot k (shard-local, grad dtype).  For tests and tools.                     */
+/* cm_set_param -- tuning knobs used by benchmarks and ablations (defaults are the
+ * measured best); CM_ERR_ARG for an unknown key or out-of-range value.
+ *   "adamw_impl"          0: 128-bit vectorised loads/stores (default), 1: TMA bulk-copy staged
+ *   "tma_blocks"          grid of the TMA AdamW kernel (default: one block per SM)
+ *   "ar_blocks_tap_only"  grid cap of the all-reduce kernel at n == 1, where it is only the
+ *                         PCIe-bound tap (default 32: leaves SMs to the shadow and training)
+ *   "shadow_blocks"       grid cap of the vectorised shadow AdamW                          */
+cm_status cm_set_param(cm_ctx *ctx, const char *key, int64_t value);
+
+/* cm_timing -- per-kernel device timing with CUDA events recorded on each kernel's own
+ * stream around its launch (after any stream waits).  enable=1 clears and starts
+ * collecting; enable=0 stops, synchronises the events and returns the summed
+ * milliseconds and launch counts per class into ms_out[5] / count_out[5] (either may be
+ * NULL): 0 all-reduce+tap kernel, 1 training AdamW, 2 shadow AdamW, 3 gradient
+ * generation, 4 restore copy.  Used by bench.py for the roofline of each kernel.        */
+cm_status cm_timing(cm_ctx *ctx, int32_t enable, double *ms_out, int64_t *count_out);
 cm_status cm_shadow_view(const cm_ctx *ctx, int32_t half, float **p, float **m, float **v);
 cm_status cm_ring_view(const cm_ctx *ctx, int32_t slot, void **grads);
 

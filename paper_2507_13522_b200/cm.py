@@ -19,12 +19,13 @@ CM_SHADOW_HOST, CM_SHADOW_DEVICE = 0, 1
 CM_FLAG_NO_TAP = 1 << 0
 CM_FLAG_ATTACH = 1 << 1
 CM_FLAG_TAP_COPYENGINE = 1 << 2
+CM_FLAG_NO_SHADOW = 1 << 3
 
 # every symbol include/cm.h declares (tests check the library exports all of them)
 EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
            "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step",
            "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_get_info",
-           "cm_bucket_info", "cm_shadow_view", "cm_ring_view"]
+           "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_set_param"]
 
 
 class cm_config(C.Structure):
@@ -89,6 +90,8 @@ def lib():
         L.cm_bucket_info.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.cm_shadow_view.argtypes = [P, C.c_int32, C.POINTER(P), C.POINTER(P), C.POINTER(P)]
         L.cm_ring_view.argtypes = [P, C.c_int32, C.POINTER(P)]
+        L.cm_set_param.argtypes = [P, C.c_char_p, C.c_int64]
+        L.cm_timing.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         for name in EXPORTS:
             if name not in ("cm_blob_size", "cm_last_error"):
                 getattr(L, name).restype = C.c_int     # cm_status
@@ -211,6 +214,16 @@ class Context:
         g = C.c_void_p()
         self._check(lib().cm_ring_view(self._ctx, int(slot), C.byref(g)))
         return g.value
+
+    def set_param(self, key, value):
+        self._check(lib().cm_set_param(self._ctx, key.encode(), int(value)))
+
+    def timing(self, enable):
+        """enable=True starts per-kernel timing; enable=False returns (ms[5], counts[5])."""
+        ms = (C.c_double * 5)()
+        cnt = (C.c_int64 * 5)()
+        self._check(lib().cm_timing(self._ctx, 1 if enable else 0, ms, cnt))
+        return list(ms), list(cnt)
 
     def finalize(self):
         if self._ctx:

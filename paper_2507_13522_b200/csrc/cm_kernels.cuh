@@ -385,6 +385,139 @@ __global__ void __launch_bounds__(kAdamThreads) adamw_kernel(const AdamParams P)
     }
 }
 
+// ------------------------------------------------------------------ AdamW, TMA-staged
+// Same arithmetic as adamw_kernel; data movement by the bulk-copy engine (TMA, 1-D
+// cp.async.bulk): one elected thread streams tiles of g, p, m, v into a kTmaStages-deep
+// shared-memory ring (mbarrier complete_tx), all threads update p/m/v in shared memory,
+// and the same thread bulk-stores the three result tiles.  Few threads, many bytes in
+// flight (kTmaStages x tile) per SM, no per-thread address arithmetic on the HBM stream.
+constexpr int kTmaThreads = 256;
+constexpr int kTmaTile = 4096;          // elements per tile
+constexpr int kTmaStages = 3;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}"
+        :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gmem_dst, const void* smem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(gmem_dst), "r"(smem_u32(smem_src)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <typename G>
+struct TmaTile {
+    static constexpr int kGBytes = kTmaTile * GT<G>::kBytes;
+    static constexpr int kStageBytes = kGBytes + 3 * kTmaTile * 4;
+};
+
+template <typename G>
+__global__ void __launch_bounds__(kTmaThreads, 1) adamw_tma_kernel(const AdamParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[kTmaStages];
+    constexpr int GB = GT<G>::kBytes;
+    const int64_t ntiles = (P.n + kTmaTile - 1) / kTmaTile;
+    auto stage_ptr = [&](int st) { return smem + (size_t)st * TmaTile<G>::kStageBytes; };
+    auto issue = [&](int64_t tile, int st) {
+        const int64_t e0 = tile * kTmaTile;
+        const int64_t len = (P.n - e0) < kTmaTile ? (P.n - e0) : kTmaTile;
+        unsigned char* b = stage_ptr(st);
+        const uint32_t gbytes = (uint32_t)(len * GB), fbytes = (uint32_t)(len * 4);
+        mbar_expect_tx(&bars[st], gbytes + 3 * fbytes);
+        bulk_load(b, (const char*)P.g + e0 * GB, gbytes, &bars[st]);
+        bulk_load(b + TmaTile<G>::kGBytes, P.p_in + e0, fbytes, &bars[st]);
+        bulk_load(b + TmaTile<G>::kGBytes + kTmaTile * 4, P.m_in + e0, fbytes, &bars[st]);
+        bulk_load(b + TmaTile<G>::kGBytes + 2 * kTmaTile * 4, P.v_in + e0, fbytes, &bars[st]);
+    };
+    const bool leader = threadIdx.x == 0;
+    if (leader) {
+        for (int st = 0; st < kTmaStages; ++st) mbar_init(&bars[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (leader) {
+        for (int st = 0; st < kTmaStages; ++st) {
+            const int64_t tile = blockIdx.x + (int64_t)st * gridDim.x;
+            if (tile < ntiles) issue(tile, st);
+        }
+    }
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % kTmaStages;
+        const uint32_t phase = (uint32_t)((it / kTmaStages) & 1);
+        mbar_wait(&bars[st], phase);
+        const int64_t e0 = tile * kTmaTile;
+        const int len = (int)((P.n - e0) < kTmaTile ? (P.n - e0) : kTmaTile);
+        unsigned char* b = stage_ptr(st);
+        float* sp = reinterpret_cast<float*>(b + TmaTile<G>::kGBytes);
+        float* sm = sp + kTmaTile;
+        float* sv = sm + kTmaTile;
+        for (int q = threadIdx.x * 4; q < len; q += kTmaThreads * 4) {
+            float4 g;
+            if constexpr (std::is_same<G, F32Tag>::value) {
+                g = *reinterpret_cast<const float4*>(b + q * 4);
+            } else {
+                const uint2 w = *reinterpret_cast<const uint2*>(b + q * 2);
+                g = make_float4(bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y));
+            }
+            float4 p = *reinterpret_cast<float4*>(sp + q);
+            float4 m = *reinterpret_cast<float4*>(sm + q);
+            float4 v = *reinterpret_cast<float4*>(sv + q);
+            adamw_elem(g.x, P.s, p.x, m.x, v.x);
+            adamw_elem(g.y, P.s, p.y, m.y, v.y);
+            adamw_elem(g.z, P.s, p.z, m.z, v.z);
+            adamw_elem(g.w, P.s, p.w, m.w, v.w);
+            *reinterpret_cast<float4*>(sp + q) = p;
+            *reinterpret_cast<float4*>(sm + q) = m;
+            *reinterpret_cast<float4*>(sv + q) = v;
+        }
+        fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the bulk copy
+        __syncthreads();
+        if (leader) {
+            const uint32_t fbytes = (uint32_t)len * 4;
+            bulk_store(P.p_out + e0, sp, fbytes);
+            bulk_store(P.m_out + e0, sm, fbytes);
+            bulk_store(P.v_out + e0, sv, fbytes);
+            bulk_commit();
+            const int64_t next = tile + (int64_t)kTmaStages * gridDim.x;
+            if (next < ntiles) {
+                bulk_wait_read0();  // the stores have read this stage; reuse it
+                issue(next, st);
+            }
+        }
+    }
+    if (leader) bulk_wait0();
+    if (P.hp_rec && blockIdx.x == 0 && threadIdx.x == 0) {
+        const float* sf = &P.s.c1;
+        for (int k = 0; k < 10; ++k) P.hp_rec[k] = sf[k];
+        __threadfence_system();
+        *P.hp_tag = P.step;
+    }
+}
+
 // ------------------------------------------------------------------ shard gather/scatter
 // Shard-local index j of rank r <-> flat index off_b + r*E_b/n + (j - shard_off_b).
 // dir 0 (snapshot): flat device p/m/v of this rank -> shard-local dst arrays.

@@ -40,6 +40,8 @@ namespace {
 constexpr uint64_t kMagic = 0x434B4D5442323030ull;  // "CKMTB200"
 constexpr uint32_t kVersion = 1;
 constexpr size_t kAlign = 4096;
+constexpr int kStages = 4;                       // shadow staging buffers
+constexpr int64_t kStageElems = 8ll << 20;       // elements per shadow staging chunk
 
 struct SegHeader {
     uint64_t magic;
@@ -99,7 +101,7 @@ struct cm_ctx {
     std::string shm_name;
     std::string err;
     int n = 1, rank = 0, dev = 0, D = 2, dtype = 0, es = 4;
-    bool no_tap = false, attach = false, ce_tap = false;
+    bool no_tap = false, attach = false, ce_tap = false, no_shadow = false;
     int shadow_place = CM_SHADOW_HOST;
     int sms = 148;
     bool cuda_dead = false;
@@ -131,6 +133,9 @@ struct cm_ctx {
 
     // launch geometry
     int ar_blocks_max = 296, adam_blocks = 1184, shadow_blocks = 296, misc_blocks = 1184;
+    int ar_blocks_tap_only = 32;   // n == 1: the kernel is only the PCIe tap; leave SMs free
+    int adamw_impl = 0;            // 0 vectorised LDG/STG (measured faster), 1 TMA bulk-copy staged
+    int tma_blocks = 148;
 
     // shadow segment
     int shm_fd = -1;
@@ -139,9 +144,13 @@ struct cm_ctx {
     bool seg_registered = false;
     char* seg_dev = nullptr;      // device alias of the mapped segment
     SegHeader* hdr = nullptr;
-    float* state_dev_alloc = nullptr;   // DEVICE placement halves
-    float* st[2][3] = {};               // host-visible pointers of halves (HOST) / device (DEVICE)
-    float* st_dev[2][3] = {};           // device-usable pointers of halves
+    // The shadow's working state lives in HBM as two ping-pong halves (half s&1 holds step
+    // s) outside the training buffers; with HOST placement every step is also persisted to
+    // the matching host half in the shm segment (write-through), so the host copy alone
+    // survives the process and the GPU.
+    float* state_dev_alloc = nullptr;
+    float* sd[2][3] = {};               // HBM halves {p, m, v}
+    float* sh[2][3] = {};               // host halves (HOST placement), nullptr otherwise
 
     // iteration bookkeeping
     int64_t cur_iter = 0;
@@ -158,6 +167,19 @@ struct cm_ctx {
     int64_t pw_s = 0;
 
     int64_t launches = 0;
+
+    // copy-engine staging of the shadow step (shadow_step_enqueue)
+    bool stg_ready = false;
+    cudaStream_t cs_h2d = nullptr, cs_d2h = nullptr, cs_k = nullptr;
+    int64_t stg_elems = 0;
+    void* stg_g[4] = {};
+    cudaEvent_t ev_stg_free[4] = {}, ev_stg_ready[4] = {}, ev_fork = nullptr, ev_join = nullptr;
+
+    // optional per-kernel timing (cm_timing): event pairs on the launching stream
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> timed;  // (class, (start, end))
 };
 
 // ====================================================================== helpers
@@ -283,11 +305,20 @@ static void launch_ar_t(int n, dim3 grid, cudaStream_t s, const ArParams& P) {
 }
 
 static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaStream_t s) {
-    int64_t items = P.n / 8;
-    int64_t want = (items + kAdamThreads - 1) / kAdamThreads;
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, blocks));
-    if (c->dtype == CM_F32) adamw_kernel<F32Tag><<<grid, kAdamThreads, 0, s>>>(P);
-    else adamw_kernel<BF16Tag><<<grid, kAdamThreads, 0, s>>>(P);
+    if (c->adamw_impl == 1) {
+        const int64_t tiles = (P.n + kTmaTile - 1) / kTmaTile;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->tma_blocks));
+        if (c->dtype == CM_F32)
+            adamw_tma_kernel<F32Tag><<<grid, kTmaThreads, kTmaStages * TmaTile<F32Tag>::kStageBytes, s>>>(P);
+        else
+            adamw_tma_kernel<BF16Tag><<<grid, kTmaThreads, kTmaStages * TmaTile<BF16Tag>::kStageBytes, s>>>(P);
+    } else {
+        int64_t items = P.n / 8;
+        int64_t want = (items + kAdamThreads - 1) / kAdamThreads;
+        int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, blocks));
+        if (c->dtype == CM_F32) adamw_kernel<F32Tag><<<grid, kAdamThreads, 0, s>>>(P);
+        else adamw_kernel<BF16Tag><<<grid, kAdamThreads, 0, s>>>(P);
+    }
     c->launches++;
     CHECK_LAUNCH();
     return CM_OK;
@@ -319,8 +350,68 @@ static T* to_dev(cm_ctx* c, T* host) {
     return (T*)(c->seg_dev + ((char*)host - c->seg));
 }
 
+// per-kernel timing: classes 0 all-reduce (rs_tap_ag), 1 train AdamW, 2 shadow AdamW,
+// 3 input generation, 4 restore copy
+static cudaEvent_t timing_event(cm_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+struct TimedScope {
+    cm_ctx* c; int cls; cudaStream_t s; cudaEvent_t a = nullptr;
+    TimedScope(cm_ctx* c_, int cls_, cudaStream_t s_) : c(c_), cls(cls_), s(s_) {
+        if (c->timing && (a = timing_event(c))) cudaEventRecord(a, s);
+    }
+    ~TimedScope() {
+        if (!a) return;
+        cudaEvent_t b = timing_event(c);
+        if (!b) return;
+        cudaEventRecord(b, s);
+        c->timed.push_back({cls, {a, b}});
+    }
+};
+
 // ====================================================================== C ABI
 extern "C" {
+
+cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
+    if (!c || !key) return CM_ERR_ARG;
+    const std::string k = key;
+    if (k == "adamw_impl" && (value == 0 || value == 1)) c->adamw_impl = (int)value;
+    else if (k == "ar_blocks_tap_only" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_tap_only = (int)value;
+    else if (k == "shadow_blocks" && value >= 1 && value <= 65535) c->shadow_blocks = (int)value;
+    else if (k == "tma_blocks" && value >= 1 && value <= 65535) c->tma_blocks = (int)value;
+    else return fail(c, CM_ERR_ARG, "unknown parameter %s=%lld", key, (long long)value);
+    return CM_OK;
+}
+
+cm_status cm_timing(cm_ctx* c, int32_t enable, double* ms_out, int64_t* count_out) {
+    if (!c) return CM_ERR_ARG;
+    if (enable) {
+        c->timing = true;
+        c->timed.clear();
+        c->ev_used = 0;
+        return CM_OK;
+    }
+    c->timing = false;
+    double ms[5] = {0, 0, 0, 0, 0};
+    int64_t cnt[5] = {0, 0, 0, 0, 0};
+    for (auto& t : c->timed) {
+        CU(cudaEventSynchronize(t.second.second));
+        float x = 0;
+        CU(cudaEventElapsedTime(&x, t.second.first, t.second.second));
+        ms[t.first] += x;
+        cnt[t.first]++;
+    }
+    if (ms_out) memcpy(ms_out, ms, sizeof ms);
+    if (count_out) memcpy(count_out, cnt, sizeof cnt);
+    c->timed.clear();
+    c->ev_used = 0;
+    return CM_OK;
+}
 
 size_t cm_blob_size(void) { return sizeof(Blob); }
 
@@ -359,6 +450,7 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
     c->dev = cfg->device;
     c->D = cfg->ring_depth;
     c->no_tap = no_tap;
+    c->no_shadow = (cfg->flags & CM_FLAG_NO_SHADOW) != 0 && !no_tap;
     c->attach = (cfg->flags & CM_FLAG_ATTACH) != 0;
     c->ce_tap = (cfg->flags & CM_FLAG_TAP_COPYENGINE) != 0;
     c->shadow_place = cfg->shadow_place;
@@ -435,6 +527,11 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
     c->adam_blocks = c->sms * std::max(aocc, 1);
     c->shadow_blocks = c->sms * 2;
     c->misc_blocks = c->sms * 4;
+    c->tma_blocks = c->sms;     // one 192 KB-smem block per SM
+    CU(cudaFuncSetAttribute(adamw_tma_kernel<F32Tag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kTmaStages * TmaTile<F32Tag>::kStageBytes));
+    CU(cudaFuncSetAttribute(adamw_tma_kernel<BF16Tag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kTmaStages * TmaTile<BF16Tag>::kStageBytes));
 
     // exchange blob
     Blob b{};
@@ -545,7 +642,7 @@ static cm_status snapshot_state(cm_ctx* c, int half, cudaStream_t s) {
     // shard r of this rank's p/m/v -> shadow half `half` (shard-local), one kernel
     ShardCopyParams P{};
     P.src[0] = c->p; P.src[1] = c->m; P.src[2] = c->v;
-    for (int a = 0; a < 3; ++a) P.dst[a][0] = c->st_dev[half][a];
+    for (int a = 0; a < 3; ++a) P.dst[a][0] = c->sd[half][a];
     P.buckets = c->d_buckets;
     P.nb = (int)c->buckets.size();
     P.n = c->n;
@@ -580,7 +677,8 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
     h.flags_off = align_up(h.meta_off + sizeof(SlotMeta) * c->D, kAlign);
     h.ring_off = align_up(h.flags_off + sizeof(uint64_t) * nb * c->D, kAlign);
     h.state_off = align_up(h.ring_off + (size_t)c->D * c->shard_numel * c->es, kAlign);
-    const size_t state_bytes = c->shadow_place == CM_SHADOW_HOST ? 6 * (size_t)c->shard_numel * 4 : 0;
+    const size_t state_bytes =
+        (c->shadow_place == CM_SHADOW_HOST && !c->no_shadow) ? 6 * (size_t)c->shard_numel * 4 : 0;
     h.total = align_up(h.state_off + state_bytes, kAlign);
 
     if (c->attach) {
@@ -619,25 +717,25 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
     CU(cudaHostRegister(c->seg, c->seg_size, cudaHostRegisterMapped | cudaHostRegisterPortable));
     c->seg_registered = true;
     CU(cudaHostGetDevicePointer((void**)&c->seg_dev, c->seg, 0));
+    if (c->no_shadow) return CM_OK;   // tap-only benchmark mode: ring + flags, no replica
     if (c->shadow_place == CM_SHADOW_HOST) {
         float* base = (float*)(c->seg + c->hdr->state_off);
         for (int hf = 0; hf < 2; ++hf)
-            for (int a = 0; a < 3; ++a) {
-                c->st[hf][a] = base + ((size_t)hf * 3 + a) * c->shard_numel;
-                c->st_dev[hf][a] = to_dev(c, c->st[hf][a]);
-            }
-    } else {
-        if (c->attach) return fail(c, CM_ERR_STATE, "DEVICE-placed shadow cannot be attached after a restart");
-        CU(cudaMalloc(&c->state_dev_alloc, 6 * (size_t)c->shard_numel * 4));
-        for (int hf = 0; hf < 2; ++hf)
-            for (int a = 0; a < 3; ++a)
-                c->st[hf][a] = c->st_dev[hf][a] = c->state_dev_alloc + ((size_t)hf * 3 + a) * c->shard_numel;
+            for (int a = 0; a < 3; ++a) c->sh[hf][a] = base + ((size_t)hf * 3 + a) * c->shard_numel;
+    } else if (c->attach) {
+        return fail(c, CM_ERR_STATE, "DEVICE-placed shadow cannot be attached after a restart");
     }
+    CU(cudaMalloc(&c->state_dev_alloc, 6 * (size_t)c->shard_numel * 4));
+    for (int hf = 0; hf < 2; ++hf)
+        for (int a = 0; a < 3; ++a) c->sd[hf][a] = c->state_dev_alloc + ((size_t)hf * 3 + a) * c->shard_numel;
     if (!c->attach) {
         // reading R19: the shadow starts as a copy of the step-0 training state
         CU(cudaDeviceSynchronize());
         cm_status s = snapshot_state(c, 0, 0);
         if (s != CM_OK) return s;
+        if (c->shadow_place == CM_SHADOW_HOST)
+            for (int a = 0; a < 3; ++a)
+                CU(cudaMemcpy(c->sh[0][a], c->sd[0][a], (size_t)c->shard_numel * 4, cudaMemcpyDeviceToHost));
         CU(cudaDeviceSynchronize());
         c->hdr->half_step[0] = 0;
         c->hdr->shadow_step = 0;
@@ -663,7 +761,12 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     }
     if (c->issued[bucket]) return fail(c, CM_ERR_STATE, "bucket %d of iteration %lld issued twice", bucket, (long long)t);
     const int slot = (int)(t % c->D);
-    if (!c->no_tap && c->issued_count == 0 && t >= c->D) {
+    if (c->no_tap && c->n == 1) {          // nothing to reduce, gather or tap
+        c->issued[bucket] = 1;
+        c->issued_count++;
+        return CM_OK;
+    }
+    if (!c->no_tap && !c->no_shadow && c->issued_count == 0 && t >= c->D) {
         // lossless flow control: slot t mod D must have been consumed by the shadow's
         // step t-D+1 (backpressure, never drop or overwrite)
         if (c->shadow_enq < t - c->D + 1)
@@ -686,7 +789,8 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     const bool kernel_tap = !c->no_tap && !c->ce_tap;
     P.tap = kernel_tap ? ring_slot_dev(c, slot) + B.shard_off * c->es : nullptr;
     const int64_t want = (P.nvec + (int64_t)kArThreads * kArUnroll - 1) / ((int64_t)kArThreads * kArUnroll);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c->ar_blocks_max));
+    const int cap_blocks = c->n == 1 ? std::min(c->ar_blocks_tap_only, c->ar_blocks_max) : c->ar_blocks_max;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap_blocks));
     if (kernel_tap) {
         P.done_ctr = c->d_done_ctr;
         c->done_total += (unsigned long long)grid;
@@ -694,8 +798,11 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         P.tap_flag = to_dev(c, slot_flags(c, slot) + bucket);
         P.tap_flag_value = (uint64_t)(t + 1);
     }
-    if (c->dtype == CM_F32) launch_ar_t<F32Tag>(c->n, grid, s, P);
-    else launch_ar_t<BF16Tag>(c->n, grid, s, P);
+    {
+        TimedScope ts(c, 0, s);
+        if (c->dtype == CM_F32) launch_ar_t<F32Tag>(c->n, grid, s, P);
+        else launch_ar_t<BF16Tag>(c->n, grid, s, P);
+    }
     c->launches++;
     CHECK_LAUNCH();
     if (!c->no_tap && c->ce_tap) {
@@ -736,25 +843,89 @@ cm_status cm_apply_step(cm_ctx* c, int64_t step, const cm_adamw* hp, void* strea
         P.hp_tag = to_dev(c, &sm->step_tag);
         P.step = step;
     }
-    cm_status st = launch_adamw(c, P, c->adam_blocks, S(stream));
+    cm_status st;
+    {
+        TimedScope ts(c, 1, S(stream));
+        st = launch_adamw(c, P, c->adam_blocks, S(stream));
+    }
     if (st != CM_OK) return st;
     c->train_step = step;
+    return CM_OK;
+}
+
+// Shadow step s on rank r's shard (shard-local arrays of L elements).  Chunks of
+// kStageElems elements pipeline through kStages staging buffers:
+//   copy engine H2D : ring slot (s-1) mod D (host) -> staging          (sizeof(G) B/elem)
+//   AdamW kernel    : HBM half (s-1)&1 -> HBM half s&1                 (28/26 B/elem HBM)
+//   copy engine D2H : HBM half s&1 -> host half s&1 (HOST placement)   (12 B/elem)
+// then the step is published in the segment header.  No SM ever waits on PCIe latency
+// (an SM zero-copy variant measured 15 GB/s); the host link carries only the bytes that
+// must persist.
+static cm_status ensure_staging(cm_ctx* c) {
+    if (c->stg_ready) return CM_OK;
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&c->cs_h2d, cudaStreamNonBlocking, lo));   // lo = least priority
+    CU(cudaStreamCreateWithPriority(&c->cs_d2h, cudaStreamNonBlocking, lo));
+    CU(cudaStreamCreateWithPriority(&c->cs_k, cudaStreamNonBlocking, lo));
+    c->stg_elems = std::min<int64_t>(kStageElems, std::max<int64_t>(c->shard_numel, 8));
+    for (int j = 0; j < kStages; ++j) {
+        CU(cudaMalloc(&c->stg_g[j], (size_t)c->stg_elems * c->es));
+        CU(cudaEventCreateWithFlags(&c->ev_stg_free[j], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->ev_stg_ready[j], cudaEventDisableTiming));
+    }
+    CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    c->stg_ready = true;
     return CM_OK;
 }
 
 static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars& a, cudaStream_t s) {
     const int slot = (int)((step - 1) % c->D);
     const int hin = (int)((step - 1) & 1), hout = (int)(step & 1);
-    cm_status st = publish(c, &c->hdr->half_step[hout], -1, s);   // half being rewritten
+    cm_status st = ensure_staging(c);
     if (st != CM_OK) return st;
-    AdamParams P{};
-    P.g = ring_slot_dev(c, slot);
-    P.p_in = c->st_dev[hin][0]; P.m_in = c->st_dev[hin][1]; P.v_in = c->st_dev[hin][2];
-    P.p_out = c->st_dev[hout][0]; P.m_out = c->st_dev[hout][1]; P.v_out = c->st_dev[hout][2];
-    P.n = c->shard_numel;
-    P.s = a;
-    st = launch_adamw(c, P, c->shadow_blocks, s);
+    st = publish(c, &c->hdr->half_step[hout], -1, s);   // half being rewritten
     if (st != CM_OK) return st;
+    const bool host = c->shadow_place == CM_SHADOW_HOST;
+    const char* ring = ring_slot_host(c, slot);
+    {
+        TimedScope ts(c, 2, s);
+        CU(cudaEventRecord(c->ev_fork, s));
+        CU(cudaStreamWaitEvent(c->cs_h2d, c->ev_fork, 0));
+        CU(cudaStreamWaitEvent(c->cs_k, c->ev_fork, 0));
+        CU(cudaStreamWaitEvent(c->cs_d2h, c->ev_fork, 0));
+        const int64_t L = c->shard_numel, C = c->stg_elems;
+        for (int64_t lo = 0, i = 0; lo < L; lo += C, ++i) {
+            const int j = (int)(i % kStages);
+            const int64_t len = std::min(C, L - lo);
+            // copy engine H2D of the ring chunk into staging j (once the kernel that used
+            // staging j kStages chunks ago is done)
+            CU(cudaStreamWaitEvent(c->cs_h2d, c->ev_stg_free[j], 0));
+            CU(cudaMemcpyAsync(c->stg_g[j], ring + lo * c->es, (size_t)len * c->es, cudaMemcpyHostToDevice,
+                               c->cs_h2d));
+            CU(cudaEventRecord(c->ev_stg_ready[j], c->cs_h2d));
+            // AdamW on its own stream: a kernel delayed by busy SMs does not stall the copies
+            CU(cudaStreamWaitEvent(c->cs_k, c->ev_stg_ready[j], 0));
+            AdamParams P{};
+            P.g = c->stg_g[j];
+            P.n = len;
+            P.s = a;
+            P.p_in = c->sd[hin][0] + lo; P.m_in = c->sd[hin][1] + lo; P.v_in = c->sd[hin][2] + lo;
+            P.p_out = c->sd[hout][0] + lo; P.m_out = c->sd[hout][1] + lo; P.v_out = c->sd[hout][2] + lo;
+            st = launch_adamw(c, P, c->shadow_blocks, c->cs_k);
+            if (st != CM_OK) return st;
+            CU(cudaEventRecord(c->ev_stg_free[j], c->cs_k));
+            if (host) {   // copy engine D2H of the new state chunk into host half s&1
+                CU(cudaStreamWaitEvent(c->cs_d2h, c->ev_stg_free[j], 0));
+                for (int k = 0; k < 3; ++k)
+                    CU(cudaMemcpyAsync(c->sh[hout][k] + lo, c->sd[hout][k] + lo, (size_t)len * 4,
+                                       cudaMemcpyDeviceToHost, c->cs_d2h));
+            }
+        }
+        CU(cudaEventRecord(c->ev_join, host ? c->cs_d2h : c->cs_k));
+        CU(cudaStreamWaitEvent(s, c->ev_join, 0));
+    }
     st = publish(c, &c->hdr->half_step[hout], step, s);
     if (st != CM_OK) return st;
     return publish(c, &c->hdr->shadow_step, step, s);
@@ -764,7 +935,7 @@ cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
     if (!c) return CM_ERR_ARG;
     if (c->cuda_dead) return CM_ERR_CUDA;
     if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
-    if (c->no_tap) return fail(c, CM_ERR_STATE, "context has no shadow (CM_FLAG_NO_TAP)");
+    if (c->no_tap || c->no_shadow) return fail(c, CM_ERR_STATE, "context has no shadow (CM_FLAG_NO_TAP/NO_SHADOW)");
     if (step != c->shadow_enq + 1)
         return fail(c, CM_ERR_STATE, "shadow step %lld after %lld: iteration gap", (long long)step, (long long)c->shadow_enq);
     const int slot = (int)((step - 1) % c->D);
@@ -792,6 +963,7 @@ cm_status cm_gen_grads(cm_ctx* c, uint64_t seed, int64_t t, int32_t scale, void*
     }();
     const int64_t nvec = c->P_pad * c->es / 16;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, c->misc_blocks));
+    TimedScope ts(c, 3, S(stream));
     if (c->dtype == CM_F32)
         gen_grads_kernel<F32Tag><<<grid, 256, 0, S(stream)>>>(c->grad, nvec, c->d_buckets, (int)c->buckets.size(), K, scale);
     else
@@ -823,7 +995,7 @@ cm_status cm_init_state(cm_ctx* c, uint64_t seed, void* stream) {
 cm_status cm_verify(cm_ctx* c, int64_t* mismatch, void* stream) {
     if (!c || !mismatch) return CM_ERR_ARG;
     if (c->cuda_dead) return CM_ERR_CUDA;
-    if (!c->connected || c->no_tap) return fail(c, CM_ERR_STATE, "no shadow to verify");
+    if (!c->connected || c->no_tap || c->no_shadow) return fail(c, CM_ERR_STATE, "no shadow to verify");
     cudaStream_t s = S(stream);
     CU(cudaStreamSynchronize(s));
     CU(cudaDeviceSynchronize());
@@ -833,11 +1005,19 @@ cm_status cm_verify(cm_ctx* c, int64_t* mismatch, void* stream) {
     unsigned long long init = ~0ull;
     CU(cudaMemcpy(c->d_bad, &init, sizeof init, cudaMemcpyHostToDevice));
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->shard_numel + 255) / 256, c->misc_blocks));
-    compare_kernel<<<grid, 256, 0, s>>>(c->st_dev[h][0], c->st_dev[h][1], c->st_dev[h][2], c->p, c->m, c->v,
-                                        c->d_buckets, (int)c->buckets.size(), c->n, c->rank, c->shard_numel,
-                                        c->d_bad);
-    c->launches++;
-    CHECK_LAUNCH();
+    // the HBM working half, and (HOST placement) the persisted host half
+    for (int which = 0; which < (c->shadow_place == CM_SHADOW_HOST ? 2 : 1); ++which) {
+        const float* const* src = which == 0 ? (const float* const*)c->sd[h] : nullptr;
+        const float* hp[3];
+        if (which == 1) {
+            for (int a = 0; a < 3; ++a) hp[a] = to_dev(c, c->sh[h][a]);
+            src = hp;
+        }
+        compare_kernel<<<grid, 256, 0, s>>>(src[0], src[1], src[2], c->p, c->m, c->v, c->d_buckets,
+                                            (int)c->buckets.size(), c->n, c->rank, c->shard_numel, c->d_bad);
+        c->launches++;
+        CHECK_LAUNCH();
+    }
     unsigned long long bad = 0;
     CU(cudaMemcpyAsync(&bad, c->d_bad, sizeof bad, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
@@ -882,7 +1062,7 @@ static ShardReach reach_of(const SegHeader* h, const char* base, int D, int nb) 
 cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     if (!c || !restored) return CM_ERR_ARG;
     if (c->cuda_dead) return CM_ERR_CUDA;
-    if (!c->connected || c->no_tap) return fail(c, CM_ERR_STATE, "no shadow to restore from");
+    if (!c->connected || c->no_tap || c->no_shadow) return fail(c, CM_ERR_STATE, "no shadow to restore from");
     cudaStream_t s = S(stream);
     CU(cudaDeviceSynchronize());
     // consolidation over all shards (read-only views of the peers' segment headers)
@@ -920,6 +1100,13 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
                         (long long)R[k].lo, (long long)R[k].hi, (long long)I);
     // bring this shard to step I
     const ShardReach& me = R[c->rank];
+    const bool host = c->shadow_place == CM_SHADOW_HOST;
+    if (host) {   // the persisted host half is the source of truth: reload the HBM half
+        const int64_t src = (I == me.newest - 1) ? I : me.newest;
+        for (int a = 0; a < 3; ++a)
+            CU(cudaMemcpyAsync(c->sd[src & 1][a], c->sh[src & 1][a], (size_t)c->shard_numel * 4,
+                               cudaMemcpyHostToDevice, s));
+    }
     if (I == me.newest - 1) {
         c->hdr->half_step[me.newest & 1] = -1;   // training will recompute that step
         c->hdr->shadow_step = I;
@@ -933,10 +1120,10 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
             if (r != CM_OK) return r;
         }
     }
-    // host shadow shard -> all ranks' p/m/v (H2D + NVLink all-gather, one kernel)
+    // shadow shard (HBM half I&1) -> all ranks' p/m/v (NVLink all-gather, one kernel)
     ShardCopyParams P{};
     const int h = (int)(I & 1);
-    for (int a = 0; a < 3; ++a) P.src[a] = c->st_dev[h][a];
+    for (int a = 0; a < 3; ++a) P.src[a] = c->sd[h][a];
     for (int k = 0; k < c->n; ++k) {
         P.dst[0][k] = c->peer_p[k];
         P.dst[1][k] = c->peer_m[k];
@@ -996,9 +1183,10 @@ cm_status cm_bucket_info(const cm_ctx* c, int32_t b, int64_t* off, int64_t* padd
 
 cm_status cm_shadow_view(const cm_ctx* c, int32_t half, float** p, float** m, float** v) {
     if (!c || half < 0 || half > 1 || !c->hdr) return CM_ERR_ARG;
-    if (p) *p = c->st[half][0];
-    if (m) *m = c->st[half][1];
-    if (v) *v = c->st[half][2];
+    float* const* src = c->shadow_place == CM_SHADOW_HOST ? c->sh[half] : c->sd[half];
+    if (p) *p = src[0];
+    if (m) *m = src[1];
+    if (v) *v = src[2];
     return CM_OK;
 }
 
@@ -1030,6 +1218,19 @@ cm_status cm_finalize(cm_ctx* c) {
     if (c->d_bad) cudaFree(c->d_bad);
     for (auto e : c->ev_tap_done) cudaEventDestroy(e);
     for (auto e : c->ev_slot_free) cudaEventDestroy(e);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->stg_ready) {
+        for (int j = 0; j < kStages; ++j) {
+            cudaFree(c->stg_g[j]);
+            cudaEventDestroy(c->ev_stg_free[j]);
+            cudaEventDestroy(c->ev_stg_ready[j]);
+        }
+        cudaEventDestroy(c->ev_fork);
+        cudaEventDestroy(c->ev_join);
+        cudaStreamDestroy(c->cs_h2d);
+        cudaStreamDestroy(c->cs_d2h);
+        cudaStreamDestroy(c->cs_k);
+    }
     delete c;
     return CM_OK;
 }

@@ -1,0 +1,111 @@
+"""Worker for the multi-process GPU tests (one process per GPU, launched by
+torch.distributed.run from tests/test_gpu_multiproc.py).  Each rank runs the hot path over
+real NVLink peer memory and checks its own state bit-for-bit against the oracle.
+
+  python -m torch.distributed.run --nproc-per-node N tests/mp_worker.py <mode> <name>
+modes: parity_f32, parity_bf16, restore_soft, hardkill_phase1, hardkill_phase2
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+from paper_2507_13522_b200 import cm, harness  # noqa: E402
+from paper_2507_13522_b200 import workloads as W  # noqa: E402
+
+HP_O = dict(lr=W.HP["lr"], b1=W.HP["beta1"], b2=W.HP["beta2"], eps=W.HP["eps"], wd=W.HP["weight_decay"])
+
+
+def bits(a):
+    a = np.asarray(a)
+    return a.view(np.uint32) if a.dtype == np.float32 else a
+
+
+def t2np(t):
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def check(R, ref, what):
+    r = R.r
+    np.testing.assert_array_equal(bits(t2np(r.grad)), bits(ref.R), err_msg=f"{what}: R rank {R.rank_id}")
+    for nm, a, b in (("p", r.p, ref.p), ("m", r.m, ref.m), ("v", r.v, ref.v)):
+        np.testing.assert_array_equal(bits(t2np(a)), bits(b), err_msg=f"{what}: {nm} rank {R.rank_id}")
+    assert r.ctx.verify(R.stream) == -1, f"{what}: shadow != train on rank {R.rank_id}"
+
+
+def main():
+    mode, name = sys.argv[1], sys.argv[2]
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = dist.get_world_size()
+    dtype = cm.CM_BF16 if mode.endswith("bf16") else cm.CM_F32
+    numel = W.numels(W.c1_ragged()) + [5, 70001]
+    cap = 1 << 20
+    plan = O.Plan(numel, cap, 4 if dtype == cm.CM_F32 else 2, n)
+    ref = O.Run(plan, seed=0, dtype=dtype, gscale=W.GRAD_SCALE, hp=HP_O)
+    flags = cm.CM_FLAG_ATTACH if mode == "hardkill_phase2" else 0
+    R = harness.DistRank(numel, dtype, cap, name, 2, cm.CM_SHADOW_HOST, flags)
+    if mode.startswith("parity"):
+        for t in range(6):
+            R.step()
+            ref.step()
+            R.sync()
+            check(R, ref, f"iteration {t}")
+    elif mode == "restore_soft":
+        for _ in range(4):
+            R.step()
+        R.sync()
+        R.r.p.fill_(float("nan"))
+        torch.cuda.synchronize()
+        dist.barrier()
+        I = R.r.ctx.restore(R.stream)
+        assert I == 4, I
+        for _ in range(4):
+            ref.step()
+        R.t = I
+        for _ in range(3):
+            R.step()
+            ref.step()
+        R.sync()
+        check(R, ref, "after restore")
+    elif mode == "hardkill_phase1":
+        for _ in range(5):
+            R.step()
+        R.sync()
+        dist.barrier()
+        os._exit(0)        # die without finalize: the shadow segments stay in /dev/shm
+    elif mode == "hardkill_phase2":
+        # fresh process, garbage training state, attach to the surviving shadow segments
+        R.r.p.fill_(float("nan"))
+        R.r.m.fill_(float("nan"))
+        torch.cuda.synchronize()
+        dist.barrier()
+        I = R.r.ctx.restore(R.stream)
+        assert I == 5, I
+        for _ in range(5):
+            ref.step()
+        R.t = I
+        for _ in range(4):
+            R.step()
+            ref.step()
+        R.sync()
+        check(R, ref, "after hard-kill restore")
+    dist.barrier()
+    R.r.ctx.finalize()
+    if mode != "hardkill_phase1":
+        cm.unlink_shadow(name, R.rank_id)
+    dist.destroy_process_group()
+    print(f"rank {R.rank_id}: {mode} ok", flush=True)
+
+
+if __name__ == "__main__":
+    main()
