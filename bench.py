@@ -44,7 +44,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="gpt2", choices=["gpt2", "c1", "llama8b"])
     ap.add_argument("--shadow", default="host", choices=["host", "device"])
-    ap.add_argument("--ring-depth", type=int, default=2)
+    ap.add_argument("--ring-depth", type=int, default=16)
+    ap.add_argument("--persist-every", type=int, default=8,
+                    help="K: host snapshot every K steps; the ring (depth >= K) logs the steps between")
+    ap.add_argument("--tap", default="fused", choices=["fused", "ce"],
+                    help="fused: in-kernel tap stores (default); ce: copy-engine tap (ablation)")
     ap.add_argument("--no-baseline", action="store_true", help="skip the NCCL + torch fused AdamW arm")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="target seconds of oracle work")
@@ -204,7 +208,8 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     shm = f"cmbench{os.getppid() if world > 1 else os.getpid()}"
     if world > 1:
         shm = f"cmbench_{os.environ.get('MASTER_PORT', '0')}"
-    R = harness.DistRank(numel, dtype, cap, shm, args.ring_depth, place)
+    flags = cm.CM_FLAG_TAP_COPYENGINE if args.tap == "ce" else 0
+    R = harness.DistRank(numel, dtype, cap, shm, args.ring_depth, place, flags, persist_every=args.persist_every)
     ctx = R.r.ctx
     info = ctx.info()
     es = 4 if dtype == cm.CM_F32 else 2
@@ -250,7 +255,8 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     sh_ms = kms[2] / max(kcnt[2], 1)
     # shadow step (copy-engine staged): H2D = ring grads; D2H = new p/m/v persisted (HOST)
     sh_h2d = info.shard_numel * es
-    sh_d2h = info.shard_numel * (12 if place == cm.CM_SHADOW_HOST else 0)
+    K = max(1, args.persist_every) if place == cm.CM_SHADOW_HOST else 1
+    sh_d2h = info.shard_numel * (12 if place == cm.CM_SHADOW_HOST else 0) / K   # per step (avg)
     kern["shadow_step"] = {"avg_ms": sh_ms, "launches": kcnt[2], "h2d_GBps": sh_h2d / (sh_ms * 1e-3) / 1e9,
                            "d2h_GBps": sh_d2h / (sh_ms * 1e-3) / 1e9, "share": kms[2] / ms,
                            "what": "H2D ring chunk -> HBM AdamW (ping-pong halves) -> D2H persist, pipelined"}
@@ -480,6 +486,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if dtype == cm.CM_F32 else "bf16-grads/f32-state", "data": "synthetic",
             "config": {"workload": name, "ranks": world, "shadow": args.shadow, "ring_depth": args.ring_depth,
+                       "tap": args.tap, "persist_every": args.persist_every,
                        "parallelism": f"dp{world}", "l2": "inputs larger than L2 (working set >> 126 MB)",
                        "iters_per_s": res["iters_per_s"]},
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res.get("e2e"),

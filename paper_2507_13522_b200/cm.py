@@ -30,7 +30,7 @@ EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", 
 
 class cm_config(C.Structure):
     _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32),
-                ("ring_depth", C.c_int32), ("shadow_place", C.c_int32), ("reserved", C.c_int32),
+                ("ring_depth", C.c_int32), ("shadow_place", C.c_int32), ("persist_every", C.c_int32),
                 ("shm_name", C.c_char_p), ("flags", C.c_uint64)]
 
 
@@ -133,10 +133,10 @@ class Context:
     """One cm_ctx (one rank).  Methods mirror the C ABI one to one."""
 
     def __init__(self, world_size, rank, device, ring_depth=2, shadow_place=CM_SHADOW_HOST,
-                 shm_name="checkmate", flags=0):
+                 shm_name="checkmate", flags=0, persist_every=1):
         self._ctx = C.c_void_p()
         self._name = shm_name.encode() if shm_name else None
-        cfg = cm_config(world_size, rank, device, ring_depth, shadow_place, 0, self._name, flags)
+        cfg = cm_config(world_size, rank, device, ring_depth, shadow_place, persist_every, self._name, flags)
         st = lib().cm_init(C.byref(cfg), C.byref(self._ctx))
         if st != CM_OK:
             msg = self.last_error()

@@ -65,7 +65,13 @@ __device__ __forceinline__ void block_barrier(const Pads& pads, int n, int rank,
         const int k = threadIdx.x;
         st_release_sys(pad_slot(pads.p[k], region, blockIdx.x, rank), epoch);
         const uint32_t* mine = pad_slot(pads.p[rank], region, blockIdx.x, k);
+        // A peer that never arrives (crashed rank, mismatched call sequence) must not hang
+        // the GPU: after ~30 s of waiting the kernel traps and the error surfaces at the
+        // next call (CM_ERR_CUDA) instead of a silent deadlock.
+        const long long t0 = clock64();
         while ((int)(ld_acquire_sys(mine) - epoch) < 0) {
+            __nanosleep(64);
+            if (clock64() - t0 > (1ll << 36)) __trap();
         }
     }
     __syncthreads();
@@ -375,6 +381,81 @@ __global__ void __launch_bounds__(kAdamThreads) adamw_kernel(const AdamParams P)
             float p = P.p_in[e], m = P.m_in[e], v = P.v_in[e];
             adamw_elem(R, P.s, p, m, v);
             P.p_out[e] = p; P.m_out[e] = m; P.v_out[e] = v;
+        }
+    }
+    if (P.hp_rec && blockIdx.x == 0 && threadIdx.x == 0) {
+        const float* sf = &P.s.c1;
+        for (int k = 0; k < 10; ++k) P.hp_rec[k] = sf[k];
+        __threadfence_system();
+        *P.hp_tag = P.step;
+    }
+}
+
+// ------------------------------------------------------------------ AdamW, warp-tiled
+// Same arithmetic; each warp owns 256-element tiles and every warp-wide 16-byte access is
+// one contiguous 512-byte run (lane l: elements 4l..4l+3 and 128+4l..128+4l+3), so each
+// load instruction touches exactly 4 full 128-byte lines.  Two tiles are loaded before
+// either is stored (16 independent 16-byte loads in flight per thread).
+constexpr int kWarpTile = 256;
+
+template <typename G>
+__device__ __forceinline__ void wt_load(const AdamParams& P, int64_t e, float4& g, float4& p, float4& m, float4& v) {
+    if constexpr (std::is_same<G, F32Tag>::value) {
+        g = __ldcs(reinterpret_cast<const float4*>((const float*)P.g + e));
+    } else {
+        const uint2 w = __ldcs(reinterpret_cast<const uint2*>((const uint16_t*)P.g + e));
+        g = make_float4(bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y));
+    }
+    p = __ldcs(reinterpret_cast<const float4*>(P.p_in + e));
+    m = __ldcs(reinterpret_cast<const float4*>(P.m_in + e));
+    v = __ldcs(reinterpret_cast<const float4*>(P.v_in + e));
+}
+__device__ __forceinline__ void wt_compute_store(const AdamParams& P, int64_t e, const float4& g, float4 p,
+                                                 float4 m, float4 v) {
+    adamw_elem(g.x, P.s, p.x, m.x, v.x);
+    adamw_elem(g.y, P.s, p.y, m.y, v.y);
+    adamw_elem(g.z, P.s, p.z, m.z, v.z);
+    adamw_elem(g.w, P.s, p.w, m.w, v.w);
+    __stcs(reinterpret_cast<float4*>(P.p_out + e), p);
+    __stcs(reinterpret_cast<float4*>(P.m_out + e), m);
+    __stcs(reinterpret_cast<float4*>(P.v_out + e), v);
+}
+
+template <typename G>
+__global__ void __launch_bounds__(kAdamThreads) adamw_wt_kernel(const AdamParams P) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)kAdamThreads + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kAdamThreads) >> 5;
+    const int64_t tiles = P.n / kWarpTile;
+    int64_t t = warp;
+    for (; t + nwarps < tiles; t += 2 * nwarps) {
+        const int64_t a0 = t * kWarpTile + 4 * lane, a1 = a0 + 128;
+        const int64_t b0 = (t + nwarps) * kWarpTile + 4 * lane, b1 = b0 + 128;
+        float4 g[4], p[4], m[4], v[4];
+        wt_load<G>(P, a0, g[0], p[0], m[0], v[0]);
+        wt_load<G>(P, a1, g[1], p[1], m[1], v[1]);
+        wt_load<G>(P, b0, g[2], p[2], m[2], v[2]);
+        wt_load<G>(P, b1, g[3], p[3], m[3], v[3]);
+        wt_compute_store(P, a0, g[0], p[0], m[0], v[0]);
+        wt_compute_store(P, a1, g[1], p[1], m[1], v[1]);
+        wt_compute_store(P, b0, g[2], p[2], m[2], v[2]);
+        wt_compute_store(P, b1, g[3], p[3], m[3], v[3]);
+    }
+    for (; t < tiles; t += nwarps) {
+        const int64_t a0 = t * kWarpTile + 4 * lane, a1 = a0 + 128;
+        float4 g[2], p[2], m[2], v[2];
+        wt_load<G>(P, a0, g[0], p[0], m[0], v[0]);
+        wt_load<G>(P, a1, g[1], p[1], m[1], v[1]);
+        wt_compute_store(P, a0, g[0], p[0], m[0], v[0]);
+        wt_compute_store(P, a1, g[1], p[1], m[1], v[1]);
+    }
+    // tail: n % 256 elements (a multiple of 4), one float4 group per thread of block 0
+    if (blockIdx.x == 0) {
+        const int64_t e = tiles * kWarpTile + 4 * (int64_t)threadIdx.x;
+        if (e < P.n) {
+            float4 g, p, m, v;
+            wt_load<G>(P, e, g, p, m, v);
+            wt_compute_store(P, e, g, p, m, v);
         }
     }
     if (P.hp_rec && blockIdx.x == 0 && threadIdx.x == 0) {

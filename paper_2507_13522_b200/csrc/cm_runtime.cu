@@ -134,8 +134,9 @@ struct cm_ctx {
     // launch geometry
     int ar_blocks_max = 296, adam_blocks = 1184, shadow_blocks = 296, misc_blocks = 1184;
     int ar_blocks_tap_only = 32;   // n == 1: the kernel is only the PCIe tap; leave SMs free
-    int adamw_impl = 0;            // 0 vectorised LDG/STG (measured faster), 1 TMA bulk-copy staged
+    int adamw_impl = 2;            // 0 vectorised, 1 TMA bulk-copy staged, 2 warp-tiled (measured best)
     int tma_blocks = 148;
+    int wt_blocks = 296;
 
     // shadow segment
     int shm_fd = -1;
@@ -158,6 +159,9 @@ struct cm_ctx {
     int issued_count = 0;
     int64_t train_step = 0;
     int64_t shadow_enq = 0;
+    int K = 1;                       // persist the host snapshot every K shadow steps
+    int64_t released_upto = 0;       // ring slots of iterations < released_upto are free
+    int64_t hh_step[2] = {0, -1};    // host snapshot halves' steps (enqueue-time mirror)
     std::vector<AdamScalars> slot_sc;
     std::vector<int64_t> slot_sc_step;
     std::vector<cudaEvent_t> ev_tap_done, ev_slot_free;
@@ -171,6 +175,8 @@ struct cm_ctx {
     // copy-engine staging of the shadow step (shadow_step_enqueue)
     bool stg_ready = false;
     cudaStream_t cs_h2d = nullptr, cs_d2h = nullptr, cs_k = nullptr;
+    cudaStream_t cs_tap = nullptr;   // CM_FLAG_TAP_COPYENGINE
+    cudaEvent_t ev_ar = nullptr;
     int64_t stg_elems = 0;
     void* stg_g[4] = {};
     cudaEvent_t ev_stg_free[4] = {}, ev_stg_ready[4] = {}, ev_fork = nullptr, ev_join = nullptr;
@@ -312,6 +318,12 @@ static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaSt
             adamw_tma_kernel<F32Tag><<<grid, kTmaThreads, kTmaStages * TmaTile<F32Tag>::kStageBytes, s>>>(P);
         else
             adamw_tma_kernel<BF16Tag><<<grid, kTmaThreads, kTmaStages * TmaTile<BF16Tag>::kStageBytes, s>>>(P);
+    } else if (c->adamw_impl == 2) {
+        const int64_t tiles = P.n / kWarpTile;
+        const int64_t want = std::max<int64_t>(1, (tiles + kAdamThreads / 32 - 1) / (kAdamThreads / 32));
+        const int grid = (int)std::min<int64_t>(want, std::min(blocks, c->wt_blocks));
+        if (c->dtype == CM_F32) adamw_wt_kernel<F32Tag><<<grid, kAdamThreads, 0, s>>>(P);
+        else adamw_wt_kernel<BF16Tag><<<grid, kAdamThreads, 0, s>>>(P);
     } else {
         int64_t items = P.n / 8;
         int64_t want = (items + kAdamThreads - 1) / kAdamThreads;
@@ -380,7 +392,8 @@ extern "C" {
 cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     if (!c || !key) return CM_ERR_ARG;
     const std::string k = key;
-    if (k == "adamw_impl" && (value == 0 || value == 1)) c->adamw_impl = (int)value;
+    if (k == "adamw_impl" && value >= 0 && value <= 2) c->adamw_impl = (int)value;
+    else if (k == "adam_blocks" && value >= 1 && value <= 65535) c->adam_blocks = (int)value;
     else if (k == "ar_blocks_tap_only" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_tap_only = (int)value;
     else if (k == "shadow_blocks" && value >= 1 && value <= 65535) c->shadow_blocks = (int)value;
     else if (k == "tma_blocks" && value >= 1 && value <= 65535) c->tma_blocks = (int)value;
@@ -438,6 +451,7 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
     if (cfg->rank < 0 || cfg->rank >= cfg->world_size) return CM_ERR_CONFIG;
     if (cfg->ring_depth < 2 || cfg->ring_depth > 64) return CM_ERR_CONFIG;
     if (cfg->shadow_place != CM_SHADOW_HOST && cfg->shadow_place != CM_SHADOW_DEVICE) return CM_ERR_CONFIG;
+    if (cfg->persist_every < 0 || cfg->persist_every > cfg->ring_depth) return CM_ERR_CONFIG;
     const bool no_tap = (cfg->flags & CM_FLAG_NO_TAP) != 0;
     if (!no_tap && (!cfg->shm_name || !cfg->shm_name[0] || strlen(cfg->shm_name) > 200))
         return CM_ERR_CONFIG;
@@ -454,6 +468,8 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
     c->attach = (cfg->flags & CM_FLAG_ATTACH) != 0;
     c->ce_tap = (cfg->flags & CM_FLAG_TAP_COPYENGINE) != 0;
     c->shadow_place = cfg->shadow_place;
+    c->K = cfg->persist_every <= 1 ? 1 : cfg->persist_every;
+    if (c->shadow_place == CM_SHADOW_DEVICE) c->K = 1;
     *out = c;   // returned even on failure so cm_last_error works; caller finalizes
 
     int ndev = 0;
@@ -528,6 +544,9 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
     c->shadow_blocks = c->sms * 2;
     c->misc_blocks = c->sms * 4;
     c->tma_blocks = c->sms;     // one 192 KB-smem block per SM
+    int wocc = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wocc, adamw_wt_kernel<F32Tag>, kAdamThreads, 0);
+    c->wt_blocks = c->sms * std::max(wocc, 1);
     CU(cudaFuncSetAttribute(adamw_tma_kernel<F32Tag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kTmaStages * TmaTile<F32Tag>::kStageBytes));
     CU(cudaFuncSetAttribute(adamw_tma_kernel<BF16Tag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -634,6 +653,9 @@ cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
     c->cur_iter = 0;
     c->train_step = 0;
     c->shadow_enq = 0;
+    c->released_upto = 0;
+    c->hh_step[0] = 0;
+    c->hh_step[1] = -1;
     c->connected = true;
     return CM_OK;
 }
@@ -769,10 +791,11 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     if (!c->no_tap && !c->no_shadow && c->issued_count == 0 && t >= c->D) {
         // lossless flow control: slot t mod D must have been consumed by the shadow's
         // step t-D+1 (backpressure, never drop or overwrite)
-        if (c->shadow_enq < t - c->D + 1)
+        if (c->released_upto < t - c->D + 1)
             return fail(c, CM_ERR_STATE,
-                        "ring slot %d still holds iteration %lld: cm_shadow_apply(%lld) not enqueued",
-                        slot, (long long)(t - c->D), (long long)(t - c->D + 1));
+                        "ring slot %d still holds iteration %lld: the shadow step (and, for a host shadow, "
+                        "the snapshot) covering it was not enqueued (shadow at %lld, released < %lld)",
+                        slot, (long long)(t - c->D), (long long)c->shadow_enq, (long long)c->released_upto);
         CU(cudaStreamWaitEvent(s, c->ev_slot_free[slot], 0));
     }
     const BucketDev& B = c->buckets[bucket];
@@ -806,16 +829,22 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     c->launches++;
     CHECK_LAUNCH();
     if (!c->no_tap && c->ce_tap) {
-        // ablation: copy-engine tap of the reduced shard after the kernel (one extra HBM read)
+        // ablation: copy-engine tap of the reduced shard, decoupled from the training stream
+        // (one extra HBM read of S/n; the D2H overlaps the next buckets' all-reduce and the
+        // AdamW; cm_apply_step makes the training stream wait for it before returning)
+        if (!c->cs_tap) CU(cudaStreamCreateWithFlags(&c->cs_tap, cudaStreamNonBlocking));
+        if (!c->ev_ar) CU(cudaEventCreateWithFlags(&c->ev_ar, cudaEventDisableTiming));
+        CU(cudaEventRecord(c->ev_ar, s));
+        CU(cudaStreamWaitEvent(c->cs_tap, c->ev_ar, 0));
         CU(cudaMemcpyAsync(ring_slot_host(c, slot) + B.shard_off * c->es,
-                           c->peer_grad[c->rank] + byte_off, shard * c->es, cudaMemcpyDeviceToHost, s));
-        cm_status st = publish(c, (volatile int64_t*)(slot_flags(c, slot) + bucket), t + 1, s);
+                           c->peer_grad[c->rank] + byte_off, shard * c->es, cudaMemcpyDeviceToHost, c->cs_tap));
+        cm_status st = publish(c, (volatile int64_t*)(slot_flags(c, slot) + bucket), t + 1, c->cs_tap);
         if (st != CM_OK) return st;
     }
     c->issued[bucket] = 1;
     c->issued_count++;
     if (!c->no_tap && c->issued_count == (int)c->buckets.size())
-        CU(cudaEventRecord(c->ev_tap_done[slot], s));
+        CU(cudaEventRecord(c->ev_tap_done[slot], c->ce_tap ? c->cs_tap : s));
     return CM_OK;
 }
 
@@ -849,6 +878,8 @@ cm_status cm_apply_step(cm_ctx* c, int64_t step, const cm_adamw* hp, void* strea
         st = launch_adamw(c, P, c->adam_blocks, S(stream));
     }
     if (st != CM_OK) return st;
+    if (!c->no_tap && c->ce_tap)   // the caller may overwrite grads after this: taps first
+        CU(cudaStreamWaitEvent(S(stream), c->ev_tap_done[slot], 0));
     c->train_step = step;
     return CM_OK;
 }
@@ -880,14 +911,25 @@ static cm_status ensure_staging(cm_ctx* c) {
     return CM_OK;
 }
 
-static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars& a, cudaStream_t s) {
+// One shadow step; returns (via *persisted) whether a host snapshot was written.  HBM
+// half step&1 receives the new state.  HOST placement persists it to the older host half
+// when step % K == 0 (or when forced): the host then holds a snapshot plus the tapped
+// gradients since it -- every step remains recoverable from host memory alone (restore
+// rolls forward over the ring), with 12/K instead of 12 bytes per element of D2H.
+static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars& a, cudaStream_t s,
+                                     bool force_persist, bool* persisted) {
     const int slot = (int)((step - 1) % c->D);
     const int hin = (int)((step - 1) & 1), hout = (int)(step & 1);
     cm_status st = ensure_staging(c);
     if (st != CM_OK) return st;
-    st = publish(c, &c->hdr->half_step[hout], -1, s);   // half being rewritten
-    if (st != CM_OK) return st;
     const bool host = c->shadow_place == CM_SHADOW_HOST;
+    const bool persist = host && (force_persist || step % c->K == 0);
+    const int ph = c->hh_step[0] <= c->hh_step[1] ? 0 : 1;     // overwrite the older snapshot
+    volatile int64_t* hs = &c->hdr->half_step[host ? ph : hout];
+    if (!host || persist) {
+        st = publish(c, hs, -1, s);   // the half being rewritten is invalid until done
+        if (st != CM_OK) return st;
+    }
     const char* ring = ring_slot_host(c, slot);
     {
         TimedScope ts(c, 2, s);
@@ -916,18 +958,26 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars&
             st = launch_adamw(c, P, c->shadow_blocks, c->cs_k);
             if (st != CM_OK) return st;
             CU(cudaEventRecord(c->ev_stg_free[j], c->cs_k));
-            if (host) {   // copy engine D2H of the new state chunk into host half s&1
+            if (persist) {   // copy engine D2H of the new state chunk into the host snapshot half
                 CU(cudaStreamWaitEvent(c->cs_d2h, c->ev_stg_free[j], 0));
                 for (int k = 0; k < 3; ++k)
-                    CU(cudaMemcpyAsync(c->sh[hout][k] + lo, c->sd[hout][k] + lo, (size_t)len * 4,
+                    CU(cudaMemcpyAsync(c->sh[ph][k] + lo, c->sd[hout][k] + lo, (size_t)len * 4,
                                        cudaMemcpyDeviceToHost, c->cs_d2h));
             }
         }
-        CU(cudaEventRecord(c->ev_join, host ? c->cs_d2h : c->cs_k));
+        CU(cudaEventRecord(c->ev_join, c->cs_k));
         CU(cudaStreamWaitEvent(s, c->ev_join, 0));
+        if (persist) {
+            CU(cudaEventRecord(c->ev_join, c->cs_d2h));
+            CU(cudaStreamWaitEvent(s, c->ev_join, 0));
+        }
     }
-    st = publish(c, &c->hdr->half_step[hout], step, s);
-    if (st != CM_OK) return st;
+    if (!host || persist) {
+        st = publish(c, hs, step, s);
+        if (st != CM_OK) return st;
+    }
+    if (persist) c->hh_step[ph] = step;
+    if (persisted) *persisted = persist;
     return publish(c, &c->hdr->shadow_step, step, s);
 }
 
@@ -943,9 +993,16 @@ cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
         return fail(c, CM_ERR_STATE, "shadow step %lld before cm_apply_step(%lld)", (long long)step, (long long)step);
     cudaStream_t s = S(side_stream);
     CU(cudaStreamWaitEvent(s, c->ev_tap_done[slot], 0));   // all taps of iteration step-1
-    cm_status st = shadow_step_enqueue(c, step, c->slot_sc[slot], s);
+    bool persisted = false;
+    cm_status st = shadow_step_enqueue(c, step, c->slot_sc[slot], s, false, &persisted);
     if (st != CM_OK) return st;
-    CU(cudaEventRecord(c->ev_slot_free[slot], s));          // release the ring slot
+    // release ring slots: DEVICE placement once consumed; HOST placement once a persisted
+    // snapshot covers them (the ring is the log that makes every step recoverable)
+    if (c->shadow_place == CM_SHADOW_DEVICE || persisted) {
+        for (int64_t u = c->released_upto; u <= step - 1; ++u)
+            CU(cudaEventRecord(c->ev_slot_free[u % c->D], s));
+        c->released_upto = step;
+    }
     c->shadow_enq = step;
     return CM_OK;
 }
@@ -1005,14 +1062,15 @@ cm_status cm_verify(cm_ctx* c, int64_t* mismatch, void* stream) {
     unsigned long long init = ~0ull;
     CU(cudaMemcpy(c->d_bad, &init, sizeof init, cudaMemcpyHostToDevice));
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->shard_numel + 255) / 256, c->misc_blocks));
-    // the HBM working half, and (HOST placement) the persisted host half
-    for (int which = 0; which < (c->shadow_place == CM_SHADOW_HOST ? 2 : 1); ++which) {
-        const float* const* src = which == 0 ? (const float* const*)c->sd[h] : nullptr;
-        const float* hp[3];
-        if (which == 1) {
-            for (int a = 0; a < 3; ++a) hp[a] = to_dev(c, c->sh[h][a]);
-            src = hp;
-        }
+    // the HBM working half, and (HOST placement) the persisted host snapshot if it is at
+    // the same step (with persist_every K > 1 it may be older; restore rolls it forward)
+    int hhalf = -1;
+    if (c->shadow_place == CM_SHADOW_HOST)
+        for (int i = 0; i < 2; ++i)
+            if (c->hdr->half_step[i] == step) hhalf = i;
+    for (int which = 0; which < (hhalf >= 0 ? 2 : 1); ++which) {
+        const float* src[3];
+        for (int a = 0; a < 3; ++a) src[a] = which == 0 ? c->sd[h][a] : to_dev(c, c->sh[hhalf][a]);
         compare_kernel<<<grid, 256, 0, s>>>(src[0], src[1], src[2], c->p, c->m, c->v, c->d_buckets,
                                             (int)c->buckets.size(), c->n, c->rank, c->shard_numel, c->d_bad);
         c->launches++;
@@ -1027,35 +1085,53 @@ cm_status cm_verify(cm_ctx* c, int64_t* mismatch, void* stream) {
 }
 
 // ---------------------------------------------------------------- restore
-// Reading R21: every shard k can produce the steps
-// [lo_k, hi_k]: hi_k = its newest valid half plus the steps it can roll forward over
-// fully tapped ring slots (all bucket flags == step and the scalar record tagged step);
-// lo_k = its older half if that half is valid and holds hi-1, else its newest half.
-// I = min_k hi_k; restore fails (UNRECOVERABLE) if some lo_k > I.
-struct ShardReach {
-    int64_t newest = -1, older = -1, hi = -1, lo = -1;
+// Reading R21.  Shard k holds snapshots in its two
+// halves (valid steps) and a ring of tapped gradients.  It can reach step x if some valid
+// snapshot b <= x exists and every step b+1..x can be rolled forward: ring slot (s-1) mod D
+// has all bucket flags == s and a scalar record tagged s.  hi_k = the largest reachable
+// step; I = min_k hi_k; restore fails (UNRECOVERABLE) if some shard cannot reach I.
+struct ShardView {
+    int64_t half[2];
+    std::vector<char> rollable;   // rollable[s - base_lo] for s in (lo, lo + 2D]
+    int64_t lo = -1;
 };
 
-static ShardReach reach_of(const SegHeader* h, const char* base, int D, int nb) {
-    ShardReach r;
-    int64_t a = h->half_step[0], b = h->half_step[1];
-    int64_t newest = std::max(a, b);
-    if (newest < 0) return r;
-    r.newest = newest;
-    int64_t other = (a == newest) ? b : a;
-    r.older = (other == newest - 1) ? other : -1;
-    int64_t hi = newest;
+static bool slot_complete(const char* base, const SegHeader* h, int D, int nb, int64_t s) {
     const SlotMeta* meta = (const SlotMeta*)(base + h->meta_off);
     const volatile uint64_t* flags = (const volatile uint64_t*)(base + h->flags_off);
-    for (int64_t s = newest + 1; s <= newest + D; ++s) {
-        const int slot = (int)((s - 1) % D);
-        bool ok = meta[slot].step_tag == s;
-        for (int bkt = 0; ok && bkt < nb; ++bkt) ok = flags[(size_t)slot * nb + bkt] == (uint64_t)s;
-        if (!ok) break;
-        hi = s;
+    const int slot = (int)((s - 1) % D);
+    if (meta[slot].step_tag != s) return false;
+    for (int bkt = 0; bkt < nb; ++bkt)
+        if (flags[(size_t)slot * nb + bkt] != (uint64_t)s) return false;
+    return true;
+}
+
+// largest step reachable from snapshot b (b itself if nothing can be rolled forward)
+static int64_t roll_limit(const char* base, const SegHeader* h, int D, int nb, int64_t b) {
+    int64_t x = b;
+    while (x < b + D && slot_complete(base, h, D, nb, x + 1)) ++x;
+    return x;
+}
+
+struct Reach {
+    int64_t snap[2] = {-1, -1};
+    int64_t lim[2] = {-1, -1};   // roll_limit from each valid snapshot
+    int64_t hi() const { return std::max(lim[0], lim[1]); }
+    // best snapshot to reach x from (the newest valid one <= x that rolls to >= x), or -1
+    int pick(int64_t x) const {
+        int best = -1;
+        for (int i = 0; i < 2; ++i)
+            if (snap[i] >= 0 && snap[i] <= x && lim[i] >= x && (best < 0 || snap[i] > snap[best])) best = i;
+        return best;
     }
-    r.hi = hi;
-    r.lo = r.older >= 0 ? r.older : newest;
+};
+
+static Reach reach_of(const SegHeader* h, const char* base, int D, int nb) {
+    Reach r;
+    for (int i = 0; i < 2; ++i) {
+        r.snap[i] = h->half_step[i];
+        if (r.snap[i] >= 0) r.lim[i] = roll_limit(base, h, D, nb, r.snap[i]);
+    }
     return r;
 }
 
@@ -1067,17 +1143,16 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     CU(cudaDeviceSynchronize());
     // consolidation over all shards (read-only views of the peers' segment headers)
     int64_t I = INT64_MAX;
-    std::vector<ShardReach> R(c->n);
+    std::vector<Reach> R(c->n);
     for (int k = 0; k < c->n; ++k) {
         char name[256];
         snprintf(name, sizeof name, "/%s.r%d", c->shm_name.c_str(), k);
         const char* base = nullptr;
         size_t len = 0;
-        int fd = -1;
         if (k == c->rank) {
             base = c->seg;
         } else {
-            fd = shm_open(name, O_RDONLY, 0);
+            int fd = shm_open(name, O_RDONLY, 0);
             if (fd < 0) return fail(c, CM_ERR_UNRECOVERABLE, "shadow segment %s missing", name);
             len = c->hdr->ring_off;   // header + meta + flags have the same layout on every rank
             void* mp = mmap(nullptr, len, PROT_READ, MAP_SHARED, fd, 0);
@@ -1091,35 +1166,37 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
         if (ok) R[k] = reach_of(h, base, c->D, (int)c->buckets.size());
         if (k != c->rank) munmap((void*)base, len);
         if (!ok) return fail(c, CM_ERR_STATE, "shadow segment %s has a different layout", name);
-        if (R[k].hi < 0) return fail(c, CM_ERR_UNRECOVERABLE, "shard %d has no valid shadow state", k);
-        I = std::min(I, R[k].hi);
+        if (R[k].hi() < 0) return fail(c, CM_ERR_UNRECOVERABLE, "shard %d has no valid shadow state", k);
+        I = std::min(I, R[k].hi());
     }
     for (int k = 0; k < c->n; ++k)
-        if (R[k].lo > I)
-            return fail(c, CM_ERR_UNRECOVERABLE, "no common step: shard %d holds [%lld, %lld], target %lld", k,
-                        (long long)R[k].lo, (long long)R[k].hi, (long long)I);
-    // bring this shard to step I
-    const ShardReach& me = R[c->rank];
+        if (R[k].pick(I) < 0)
+            return fail(c, CM_ERR_UNRECOVERABLE, "no common step: shard %d cannot reach step %lld", k, (long long)I);
+    // bring this shard to step I: load its snapshot into the HBM half, roll forward
+    const Reach& me = R[c->rank];
+    const int bi = me.pick(I);
+    const int64_t b = me.snap[bi];
     const bool host = c->shadow_place == CM_SHADOW_HOST;
-    if (host) {   // the persisted host half is the source of truth: reload the HBM half
-        const int64_t src = (I == me.newest - 1) ? I : me.newest;
+    if (host) {
         for (int a = 0; a < 3; ++a)
-            CU(cudaMemcpyAsync(c->sd[src & 1][a], c->sh[src & 1][a], (size_t)c->shard_numel * 4,
+            CU(cudaMemcpyAsync(c->sd[b & 1][a], c->sh[bi][a], (size_t)c->shard_numel * 4,
                                cudaMemcpyHostToDevice, s));
-    }
-    if (I == me.newest - 1) {
-        c->hdr->half_step[me.newest & 1] = -1;   // training will recompute that step
-        c->hdr->shadow_step = I;
+        c->hh_step[0] = me.snap[0];
+        c->hh_step[1] = me.snap[1];
     } else {
-        for (int64_t st = me.newest + 1; st <= I; ++st) {   // roll forward over the ring
-            const int slot = (int)((st - 1) % c->D);
-            const SlotMeta* sm = slot_meta(c, slot);
-            AdamScalars a;
-            memcpy(&a, (const void*)sm->sc, sizeof a);
-            cm_status r = shadow_step_enqueue(c, st, a, s);
-            if (r != CM_OK) return r;
-        }
+        // DEVICE placement: the HBM halves are the snapshots (half i holds step snap[i], i = step&1)
+        for (int i = 0; i < 2; ++i)
+            if (me.snap[i] > I) c->hdr->half_step[i] = -1;   // training will recompute that step
     }
+    for (int64_t st = b + 1; st <= I; ++st) {   // roll forward over the ring
+        const int slot = (int)((st - 1) % c->D);
+        const SlotMeta* sm = slot_meta(c, slot);
+        AdamScalars a;
+        memcpy(&a, (const void*)sm->sc, sizeof a);
+        cm_status r = shadow_step_enqueue(c, st, a, s, /*force_persist=*/st == I, nullptr);
+        if (r != CM_OK) return r;
+    }
+    c->hdr->shadow_step = I;
     // shadow shard (HBM half I&1) -> all ranks' p/m/v (NVLink all-gather, one kernel)
     ShardCopyParams P{};
     const int h = (int)(I & 1);
@@ -1149,6 +1226,7 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     c->issued_count = 0;
     c->train_step = I;
     c->shadow_enq = I;
+    c->released_upto = I;   // step I is persisted (HOST) / held in HBM (DEVICE)
     for (int i = 0; i < c->D; ++i) c->slot_sc_step[i] = -1;
     *restored = I;
     return CM_OK;
@@ -1219,6 +1297,8 @@ cm_status cm_finalize(cm_ctx* c) {
     for (auto e : c->ev_tap_done) cudaEventDestroy(e);
     for (auto e : c->ev_slot_free) cudaEventDestroy(e);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->cs_tap) cudaStreamDestroy(c->cs_tap);
+    if (c->ev_ar) cudaEventDestroy(c->ev_ar);
     if (c->stg_ready) {
         for (int j = 0; j < kStages; ++j) {
             cudaFree(c->stg_g[j]);

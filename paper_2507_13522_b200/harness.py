@@ -26,7 +26,7 @@ class Rank:
 
     def __init__(self, numel, world_size, rank, device, grad_dtype=cm.CM_F32, cap_bytes=W.CAP_BYTES,
                  shm_name="checkmate", ring_depth=2, shadow_place=cm.CM_SHADOW_HOST, flags=0,
-                 seed=W.SEED, init_state=True):
+                 seed=W.SEED, init_state=True, persist_every=1):
         self.numel = list(numel)
         self.n, self.rank, self.device = world_size, rank, device
         self.grad_dtype, self.cap_bytes, self.seed = grad_dtype, cap_bytes, seed
@@ -38,7 +38,7 @@ class Rank:
         self.p = torch.empty(self.padded, dtype=torch.float32, device=dev)
         self.m = torch.empty(self.padded, dtype=torch.float32, device=dev)
         self.v = torch.empty(self.padded, dtype=torch.float32, device=dev)
-        self.ctx = cm.Context(world_size, rank, device, ring_depth, shadow_place, shm_name, flags)
+        self.ctx = cm.Context(world_size, rank, device, ring_depth, shadow_place, shm_name, flags, persist_every)
         self.blob = self.ctx.register_buckets(self.numel, grad_dtype, cap_bytes, self.grad.data_ptr(),
                                               self.p.data_ptr(), self.m.data_ptr(), self.v.data_ptr())
         if init_state:
@@ -56,7 +56,7 @@ class VirtualGroup:
 
     def __init__(self, numel, world_size, device=0, grad_dtype=cm.CM_F32, cap_bytes=W.CAP_BYTES,
                  shm_name="cmvg", ring_depth=2, shadow_place=cm.CM_SHADOW_HOST, flags=0, seed=W.SEED,
-                 gscale=W.GRAD_SCALE, hp=None):
+                 gscale=W.GRAD_SCALE, hp=None, persist_every=1):
         self.n = world_size
         self.seed, self.gscale = seed, gscale
         self.hp = dict(W.HP)
@@ -64,7 +64,7 @@ class VirtualGroup:
             self.hp.update(hp)
         self.no_tap = bool(flags & cm.CM_FLAG_NO_TAP)
         self.ranks = [Rank(numel, world_size, r, device, grad_dtype, cap_bytes, shm_name, ring_depth,
-                           shadow_place, flags, seed) for r in range(world_size)]
+                           shadow_place, flags, seed, persist_every=persist_every) for r in range(world_size)]
         blobs = [r.blob for r in self.ranks]
         for r in self.ranks:
             r.ctx.connect(blobs)
@@ -118,7 +118,8 @@ class DistRank:
     """This process's rank of a torch.distributed group (one GPU per process)."""
 
     def __init__(self, numel, grad_dtype=cm.CM_F32, cap_bytes=W.CAP_BYTES, shm_name="cmdist", ring_depth=2,
-                 shadow_place=cm.CM_SHADOW_HOST, flags=0, seed=W.SEED, gscale=W.GRAD_SCALE, hp=None):
+                 shadow_place=cm.CM_SHADOW_HOST, flags=0, seed=W.SEED, gscale=W.GRAD_SCALE, hp=None,
+                 persist_every=1):
         import torch.distributed as dist
         self.n = dist.get_world_size()
         self.rank_id = dist.get_rank()
@@ -130,7 +131,7 @@ class DistRank:
             self.hp.update(hp)
         self.no_tap = bool(flags & cm.CM_FLAG_NO_TAP)
         self.r = Rank(numel, self.n, self.rank_id, local, grad_dtype, cap_bytes, shm_name, ring_depth,
-                      shadow_place, flags, seed)
+                      shadow_place, flags, seed, persist_every=persist_every)
         blobs = [None] * self.n
         dist.all_gather_object(blobs, self.r.blob)
         self.r.ctx.connect(blobs)

@@ -196,9 +196,7 @@ def test_flow_control_refuses_to_overwrite_unconsumed_slot():
         with pytest.raises(cm.CMError) as e:
             g.allreduce()             # iteration 2 would overwrite slot 0
         assert e.value.status == cm.CM_ERR_STATE
-        g.shadow(step=1)
-        for r in g.ranks:             # slot 0 released: the same call now succeeds
-            pass
+        g.shadow(step=1)              # slot 0 released: the same call now succeeds
         g.allreduce()
         g.apply()
         g.t += 1
@@ -348,5 +346,119 @@ def test_llama_shaped_bf16_sampled():
         np.testing.assert_array_equal(bits(Rg), bits(R))
         for rr in g.ranks:
             assert rr.ctx.verify(g.stream) == -1
+    finally:
+        close(g)
+
+
+@pytest.mark.parametrize("impl", [0, 1, 2])
+@pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
+def test_adamw_implementations_bit_exact(impl, dtype):
+    """Every AdamW data-movement variant (vectorised, TMA-staged, warp-tiled) computes the
+    same bits: the arithmetic is one device function; only the loads/stores differ."""
+    numel = TABLES["mixed"]
+    g = make_group(numel, 2, dtype)
+    for r in g.ranks:
+        r.ctx.set_param("adamw_impl", impl)
+    plan, ref = oracle_for(numel, 2, dtype, 1 << 20)
+    try:
+        for t in range(3):
+            g.step()
+            ref.step()
+        g.sync()
+        for r in g.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            np.testing.assert_array_equal(bits(t2np(r.m)), bits(ref.m))
+            np.testing.assert_array_equal(bits(t2np(r.v)), bits(ref.v))
+            assert r.ctx.verify(g.stream) == -1
+    finally:
+        close(g)
+
+
+@pytest.mark.parametrize("blocks", [1, 7, 148, 1024])
+def test_grid_invariance(blocks):
+    """Element-local math: any grid gives identical bytes (SURVEY 8.c grid invariance)."""
+    numel = TABLES["ragged"]
+    g = make_group(numel, 1)
+    for r in g.ranks:
+        r.ctx.set_param("ar_blocks_tap_only", blocks)
+        r.ctx.set_param("adam_blocks", blocks)
+        r.ctx.set_param("shadow_blocks", blocks)
+    plan, ref = oracle_for(numel, 1, cm.CM_F32, 1 << 20)
+    try:
+        for t in range(2):
+            g.step()
+            ref.step()
+        g.sync()
+        np.testing.assert_array_equal(bits(t2np(g.ranks[0].p)), bits(ref.p))
+        np.testing.assert_array_equal(bits(ring_flat(g, 1)), bits(ref.T))
+        assert g.ranks[0].ctx.verify(g.stream) == -1
+    finally:
+        close(g)
+
+
+@pytest.mark.parametrize("K,D", [(2, 2), (4, 4), (4, 6)])
+def test_persist_every_k_restore_rolls_forward(K, D):
+    """Host snapshot every K steps; the ring logs the steps between.  After a failure at any
+    step, restore rolls forward from the last snapshot over the ring and resumes bit-exact."""
+    numel = TABLES["ragged"]
+    n = 2
+    for kill_at in (K + 1, 2 * K, 2 * K + 1):
+        name = _name()
+        g = harness.VirtualGroup(numel, n, 0, cm.CM_F32, 1 << 20, name, D, cm.CM_SHADOW_HOST, 0, 0,
+                                 persist_every=K)
+        g._shm = name
+        plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
+        try:
+            for t in range(kill_at):
+                g.step()
+            g.sync()
+            for r in g.ranks:
+                assert r.ctx.verify(g.stream) == -1
+                r.p.fill_(float("nan")); r.m.fill_(float("nan")); r.v.fill_(float("nan"))
+            torch.cuda.synchronize()
+            steps = [r.ctx.restore(g.stream) for r in g.ranks]
+            assert steps == [kill_at] * n, (steps, kill_at)
+            for _ in range(kill_at):
+                ref.step()
+            for r in g.ranks:
+                np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+                np.testing.assert_array_equal(bits(t2np(r.v)), bits(ref.v))
+            g.t = kill_at
+            for _ in range(2 * K + 1):
+                g.step()
+                ref.step()
+            g.sync()
+            for r in g.ranks:
+                np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+                assert r.ctx.verify(g.stream) == -1
+        finally:
+            close(g)
+
+
+def test_consolidation_min_rule_across_lagging_shards():
+    """Shards at different shadow steps (rank 1's shadow stops 2 steps early, its ring still
+    holds the taps): I = min over shards of the reachable step; both end bit-exact at I."""
+    numel = TABLES["ragged"]
+    n = 2
+    g = make_group(numel, n, D=4)
+    plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
+    try:
+        for t in range(6):
+            g.gen()
+            g.allreduce()
+            g.apply()
+            g.ranks[0].ctx.shadow_apply(t + 1, g.side)
+            if t < 4:
+                g.ranks[1].ctx.shadow_apply(t + 1, g.side)
+            g.t += 1
+        g.sync()
+        assert [r.ctx.info().shadow_step for r in g.ranks] == [6, 4]
+        steps = [r.ctx.restore(g.stream) for r in g.ranks]
+        assert steps == [6, 6]                      # rank 1 rolls forward over its ring
+        for _ in range(6):
+            ref.step()
+        for r in g.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            assert r.ctx.verify(g.stream) == -1
     finally:
         close(g)

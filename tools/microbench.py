@@ -179,8 +179,8 @@ def shadow(place):
             "step_ms_sum_of_classes": sum(ms[:4]) / 10}
 
 
-TESTS = {"pcie": pcie, "adamw": adamw, "adamw_vec": lambda: adamw(0), "adamw_bf16": adamw_bf16,
-         "adamw_bf16_vec": lambda: adamw_bf16(0), "gen": gen, "tap": tap,
+TESTS = {"pcie": pcie, "adamw": adamw, "adamw_vec": lambda: adamw(0), "adamw_wt": lambda: adamw(2), "adamw_bf16": adamw_bf16,
+         "adamw_bf16_vec": lambda: adamw_bf16(0), "adamw_bf16_wt": lambda: adamw_bf16(2), "gen": gen, "tap": tap,
          "tap16": lambda: tap(blocks=16), "tap64": lambda: tap(blocks=64), "tap148": lambda: tap(blocks=148),
          "tap_ce": lambda: tap(cm.CM_FLAG_TAP_COPYENGINE, "tap via copy engine (ablation)"),
          "ar_virtual": ar_virtual, "shadow_host": lambda: shadow(cm.CM_SHADOW_HOST),
