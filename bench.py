@@ -47,8 +47,9 @@ def parse():
     ap.add_argument("--ring-depth", type=int, default=16)
     ap.add_argument("--persist-every", type=int, default=8,
                     help="K: host snapshot every K steps; the ring (depth >= K) logs the steps between")
-    ap.add_argument("--tap", default="fused", choices=["fused", "ce"],
-                    help="fused: in-kernel tap stores (default); ce: copy-engine tap (ablation)")
+    ap.add_argument("--tap", default="staged", choices=["staged", "direct", "ce"],
+                    help="staged (default): in-kernel stores to HBM staging + copy-engine drain; direct: "
+                         "in-kernel stores straight to the host ring; ce: copy engine reads the grad buffer back")
     ap.add_argument("--no-baseline", action="store_true", help="skip the NCCL + torch fused AdamW arm")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="target seconds of oracle work")
@@ -208,7 +209,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     shm = f"cmbench{os.getppid() if world > 1 else os.getpid()}"
     if world > 1:
         shm = f"cmbench_{os.environ.get('MASTER_PORT', '0')}"
-    flags = cm.CM_FLAG_TAP_COPYENGINE if args.tap == "ce" else 0
+    flags = {"ce": cm.CM_FLAG_TAP_COPYENGINE, "direct": cm.CM_FLAG_TAP_DIRECT}.get(args.tap, 0)
     R = harness.DistRank(numel, dtype, cap, shm, args.ring_depth, place, flags, persist_every=args.persist_every)
     ctx = R.r.ctx
     info = ctx.info()

@@ -101,7 +101,9 @@ struct cm_ctx {
     std::string shm_name;
     std::string err;
     int n = 1, rank = 0, dev = 0, D = 2, dtype = 0, es = 4;
-    bool no_tap = false, attach = false, ce_tap = false, no_shadow = false;
+    bool no_tap = false, attach = false, ce_tap = false, no_shadow = false, staged_tap = false;
+    void* stage_buf[2] = {};              // default tap: HBM staging of the reduced shard
+    cudaEvent_t ev_stage_free[2] = {};
     int shadow_place = CM_SHADOW_HOST;
     int sms = 148;
     bool cuda_dead = false;
@@ -289,11 +291,26 @@ static AdamScalars make_scalars(cm_ctx* c, int64_t s, const cm_adamw& hp) {
 }
 
 // ---------------------------------------------------------------- launch helpers
-template <typename G>
-static int ar_occupancy() {
+template <typename G, int N>
+static int ar_occ_n() {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rs_tap_ag_kernel<G, 8>, kArThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rs_tap_ag_kernel<G, N>, kArThreads, 0);
     return occ > 0 ? occ : 1;
+}
+// co-resident blocks per SM of the n-rank instance (blocks pair across GPUs by index, so
+// the grid never exceeds what is resident at once)
+template <typename G>
+static int ar_occupancy(int n) {
+    switch (n) {
+        case 1: return ar_occ_n<G, 1>();
+        case 2: return ar_occ_n<G, 2>();
+        case 3: return ar_occ_n<G, 3>();
+        case 4: return ar_occ_n<G, 4>();
+        case 5: return ar_occ_n<G, 5>();
+        case 6: return ar_occ_n<G, 6>();
+        case 7: return ar_occ_n<G, 7>();
+        default: return ar_occ_n<G, 8>();
+    }
 }
 
 template <typename G>
@@ -397,6 +414,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "ar_blocks_tap_only" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_tap_only = (int)value;
     else if (k == "shadow_blocks" && value >= 1 && value <= 65535) c->shadow_blocks = (int)value;
     else if (k == "tma_blocks" && value >= 1 && value <= 65535) c->tma_blocks = (int)value;
+    else if (k == "ar_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_max = (int)value;
     else return fail(c, CM_ERR_ARG, "unknown parameter %s=%lld", key, (long long)value);
     return CM_OK;
 }
@@ -467,6 +485,8 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
     c->no_shadow = (cfg->flags & CM_FLAG_NO_SHADOW) != 0 && !no_tap;
     c->attach = (cfg->flags & CM_FLAG_ATTACH) != 0;
     c->ce_tap = (cfg->flags & CM_FLAG_TAP_COPYENGINE) != 0;
+    // default tap = staged; CM_FLAG_TAP_DIRECT = kernel stores straight into the host ring
+    c->staged_tap = (cfg->flags & CM_FLAG_TAP_DIRECT) == 0 && !c->ce_tap;
     c->shadow_place = cfg->shadow_place;
     c->K = cfg->persist_every <= 1 ? 1 : cfg->persist_every;
     if (c->shadow_place == CM_SHADOW_DEVICE) c->K = 1;
@@ -536,7 +556,7 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
                   cudaMemcpyHostToDevice));
 
     // launch geometry (identical on every rank: same GPU model, same plan)
-    int occ = c->dtype == CM_F32 ? ar_occupancy<F32Tag>() : ar_occupancy<BF16Tag>();
+    int occ = c->dtype == CM_F32 ? ar_occupancy<F32Tag>(c->n) : ar_occupancy<BF16Tag>(c->n);
     c->ar_blocks_max = std::min(c->sms * occ, kMaxBarrierBlocks);
     int aocc = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&aocc, adamw_kernel<F32Tag>, kAdamThreads, 0);
@@ -788,6 +808,9 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         c->issued_count++;
         return CM_OK;
     }
+    // n == 1 with the copy-engine tap: the reduced value is the local gradient, so no kernel
+    // runs; only the copy engine moves the bucket to the ring (below)
+    const bool skip_kernel = c->n == 1 && c->ce_tap && !c->no_tap;
     if (!c->no_tap && !c->no_shadow && c->issued_count == 0 && t >= c->D) {
         // lossless flow control: slot t mod D must have been consumed by the shadow's
         // step t-D+1 (backpressure, never drop or overwrite)
@@ -809,42 +832,64 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     P.rank = c->rank;
     P.barriers = c->barriers ? 1 : 0;
     P.ag = c->n > 1 ? 1 : 0;
-    const bool kernel_tap = !c->no_tap && !c->ce_tap;
-    P.tap = kernel_tap ? ring_slot_dev(c, slot) + B.shard_off * c->es : nullptr;
+    // tap modes: fused (kernel stores to the host ring), staged (kernel stores to an HBM
+    // staging half, a copy engine drains it to the ring), copy-engine (CE reads the reduced
+    // shard back from the grad buffer after the kernel)
+    const bool fused_tap = !c->no_tap && !c->ce_tap && !c->staged_tap;
+    const bool staged = !c->no_tap && c->staged_tap;
+    if (staged) {
+        if (!c->stage_buf[0]) {
+            for (int i = 0; i < 2; ++i) {
+                CU(cudaMalloc(&c->stage_buf[i], (size_t)c->shard_numel * c->es));
+                CU(cudaEventCreateWithFlags(&c->ev_stage_free[i], cudaEventDisableTiming));
+            }
+        }
+        if (c->issued_count == 0)   // staging half t&1 drained (iteration t-2's copies done)
+            CU(cudaStreamWaitEvent(s, c->ev_stage_free[t & 1], 0));
+    }
+    if (fused_tap) P.tap = ring_slot_dev(c, slot) + B.shard_off * c->es;
+    else if (staged) P.tap = (char*)c->stage_buf[t & 1] + B.shard_off * c->es;
     const int64_t want = (P.nvec + (int64_t)kArThreads * kArUnroll - 1) / ((int64_t)kArThreads * kArUnroll);
-    const int cap_blocks = c->n == 1 ? std::min(c->ar_blocks_tap_only, c->ar_blocks_max) : c->ar_blocks_max;
+    const int cap_blocks = (c->n == 1 && fused_tap) ? std::min(c->ar_blocks_tap_only, c->ar_blocks_max) : c->ar_blocks_max;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap_blocks));
-    if (kernel_tap) {
+    if (fused_tap) {
         P.done_ctr = c->d_done_ctr;
         c->done_total += (unsigned long long)grid;
         P.done_target = c->done_total;
         P.tap_flag = to_dev(c, slot_flags(c, slot) + bucket);
         P.tap_flag_value = (uint64_t)(t + 1);
     }
-    {
+    if (!skip_kernel) {
         TimedScope ts(c, 0, s);
         if (c->dtype == CM_F32) launch_ar_t<F32Tag>(c->n, grid, s, P);
         else launch_ar_t<BF16Tag>(c->n, grid, s, P);
+        c->launches++;
+        CHECK_LAUNCH();
     }
-    c->launches++;
-    CHECK_LAUNCH();
-    if (!c->no_tap && c->ce_tap) {
-        // ablation: copy-engine tap of the reduced shard, decoupled from the training stream
-        // (one extra HBM read of S/n; the D2H overlaps the next buckets' all-reduce and the
-        // AdamW; cm_apply_step makes the training stream wait for it before returning)
+    if (!c->no_tap && (c->ce_tap || staged)) {
+        // copy-engine drain of the reduced shard to the host ring, decoupled from the training
+        // stream: it overlaps the next buckets' all-reduce, the AdamW and (model mode) the
+        // backward.  CE mode reads the grad buffer back (cm_apply_step then waits for these
+        // copies before the caller may overwrite grads); staged mode reads the HBM staging
+        // half the kernel wrote, so the grad buffer is free as soon as the kernel is done.
         if (!c->cs_tap) CU(cudaStreamCreateWithFlags(&c->cs_tap, cudaStreamNonBlocking));
         if (!c->ev_ar) CU(cudaEventCreateWithFlags(&c->ev_ar, cudaEventDisableTiming));
         CU(cudaEventRecord(c->ev_ar, s));
         CU(cudaStreamWaitEvent(c->cs_tap, c->ev_ar, 0));
-        CU(cudaMemcpyAsync(ring_slot_host(c, slot) + B.shard_off * c->es,
-                           c->peer_grad[c->rank] + byte_off, shard * c->es, cudaMemcpyDeviceToHost, c->cs_tap));
+        const char* src = staged ? (const char*)c->stage_buf[t & 1] + B.shard_off * c->es
+                                 : c->peer_grad[c->rank] + byte_off;
+        CU(cudaMemcpyAsync(ring_slot_host(c, slot) + B.shard_off * c->es, src, shard * c->es,
+                           cudaMemcpyDeviceToHost, c->cs_tap));
         cm_status st = publish(c, (volatile int64_t*)(slot_flags(c, slot) + bucket), t + 1, c->cs_tap);
         if (st != CM_OK) return st;
     }
     c->issued[bucket] = 1;
     c->issued_count++;
-    if (!c->no_tap && c->issued_count == (int)c->buckets.size())
-        CU(cudaEventRecord(c->ev_tap_done[slot], c->ce_tap ? c->cs_tap : s));
+    if (!c->no_tap && c->issued_count == (int)c->buckets.size()) {
+        const bool via_ce = c->ce_tap || staged;
+        CU(cudaEventRecord(c->ev_tap_done[slot], via_ce ? c->cs_tap : s));
+        if (staged) CU(cudaEventRecord(c->ev_stage_free[t & 1], c->cs_tap));
+    }
     return CM_OK;
 }
 
@@ -1298,6 +1343,10 @@ cm_status cm_finalize(cm_ctx* c) {
     for (auto e : c->ev_slot_free) cudaEventDestroy(e);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->cs_tap) cudaStreamDestroy(c->cs_tap);
+    for (int i = 0; i < 2; ++i) {
+        if (c->stage_buf[i]) cudaFree(c->stage_buf[i]);
+        if (c->ev_stage_free[i]) cudaEventDestroy(c->ev_stage_free[i]);
+    }
     if (c->ev_ar) cudaEventDestroy(c->ev_ar);
     if (c->stg_ready) {
         for (int j = 0; j < kStages; ++j) {

@@ -130,12 +130,14 @@ def test_device_shadow_placement_bit_exact():
         close(g)
 
 
-def test_copy_engine_tap_ablation_bit_exact():
+@pytest.mark.parametrize("n", [1, 4])
+@pytest.mark.parametrize("flag", [cm.CM_FLAG_TAP_COPYENGINE, cm.CM_FLAG_TAP_DIRECT])
+def test_copy_engine_tap_modes_bit_exact(flag, n):
     numel = TABLES["ragged"]
-    g = make_group(numel, 4, flags=cm.CM_FLAG_TAP_COPYENGINE)
-    plan, ref = oracle_for(numel, 4, cm.CM_F32, 1 << 20)
+    g = make_group(numel, n, flags=flag)
+    plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
     try:
-        for t in range(3):
+        for t in range(5):
             g.step()
             ref.step()
             g.sync()
@@ -381,6 +383,7 @@ def test_grid_invariance(blocks):
     g = make_group(numel, 1)
     for r in g.ranks:
         r.ctx.set_param("ar_blocks_tap_only", blocks)
+        r.ctx.set_param("ar_blocks", blocks)
         r.ctx.set_param("adam_blocks", blocks)
         r.ctx.set_param("shadow_blocks", blocks)
     plan, ref = oracle_for(numel, 1, cm.CM_F32, 1 << 20)

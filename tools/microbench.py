@@ -92,7 +92,7 @@ def gen():
     return {"kernel": "gen_grads fp32", "avg_ms": avg, "write_GBps": P * 4 / (avg * 1e-3) / 1e9}
 
 
-def tap(flags=0, label="rs_tap_ag n=1 (tap only)", blocks=32):
+def tap(flags=cm.CM_FLAG_TAP_DIRECT, label="rs_tap_ag n=1 (direct tap)", blocks=32):
     """All buckets of one iteration (kernel tap, or kernel + copy-engine tap), alone: the
     shadow runs only after the timed region."""
     g = group(1, flags)
@@ -183,6 +183,7 @@ TESTS = {"pcie": pcie, "adamw": adamw, "adamw_vec": lambda: adamw(0), "adamw_wt"
          "adamw_bf16_vec": lambda: adamw_bf16(0), "adamw_bf16_wt": lambda: adamw_bf16(2), "gen": gen, "tap": tap,
          "tap16": lambda: tap(blocks=16), "tap64": lambda: tap(blocks=64), "tap148": lambda: tap(blocks=148),
          "tap_ce": lambda: tap(cm.CM_FLAG_TAP_COPYENGINE, "tap via copy engine (ablation)"),
+         "tap_staged": lambda: tap(0, "staged tap (kernel -> HBM staging, copy-engine drain)"),
          "ar_virtual": ar_virtual, "shadow_host": lambda: shadow(cm.CM_SHADOW_HOST),
          "shadow_dev": lambda: shadow(cm.CM_SHADOW_DEVICE)}
 

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--max-mib", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--ar-blocks", type=int, default=0, help="grid cap override (0 = library default)")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -52,6 +53,8 @@ def main():
             flags = cm.CM_FLAG_NO_SHADOW if args.mode == "ours_tap" else cm.CM_FLAG_NO_TAP
             name = f"cmsw_{os.environ.get('MASTER_PORT', '0')}_{mib}"
             R = harness.DistRank(numel, dtype, S + 1, name, 2, cm.CM_SHADOW_HOST, flags)
+            if args.ar_blocks:
+                R.r.ctx.set_param("ar_blocks", args.ar_blocks)
             R.r.ctx.gen_grads(0, 0, 10, R.stream)
             R.stream.synchronize()
             stream = R.stream
@@ -73,7 +76,7 @@ def main():
         med = tt.item()
         if rank == 0:
             sec = med * 1e-3
-            print(json.dumps({"mode": args.mode, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
+            print(json.dumps({"mode": args.mode, "ar_blocks": args.ar_blocks, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
                               "dtype": args.dtype, "n": n, "bytes": S, "ms": med,
                               "p10_ms": sorted(times)[len(times) // 10], "p90_ms": sorted(times)[9 * len(times) // 10],
                               "algbw_GBps": S / sec / 1e9, "busbw_GBps": 2 * (n - 1) / n * S / sec / 1e9,
