@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--no-baseline", action="store_true", help="skip the NCCL + torch fused AdamW arm")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="target seconds of oracle work")
+    ap.add_argument("--no-model", action="store_true",
+                    help="skip the GPT-2 model-mode arms (real fwd/bwd; checkpoint overhead vs NCCL DDP)")
+    ap.add_argument("--model-steps", type=int, default=10)
+    ap.add_argument("--micro-batch", type=int, default=16)
     return ap.parse_args()
 
 
@@ -474,6 +478,17 @@ def main():
     res = run_ours(args, rank, world, local, name, numel, dtype, cap)
     base = None if args.no_baseline else run_nccl_baseline(args, rank, world, local, numel, dtype, cap)
     ours_nockpt = None if args.no_baseline else run_ours_nockpt(args, rank, world, local, numel, dtype, cap)
+    model = None
+    if not args.no_model and args.workload == "gpt2":
+        import types
+        from paper_2507_13522_b200.modelbench import run_arm
+        margs = types.SimpleNamespace(steps=args.model_steps, warmup=max(3, args.warmup), micro_batch=args.micro_batch,
+                                      ring_depth=args.ring_depth, persist_every=args.persist_every, tap=args.tap)
+        model = {arm: run_arm(arm, margs, rank, world, local) for arm in ("nccl", "ours_nockpt", "ours_ckpt")}
+        model["ckpt_overhead_pct_vs_nccl"] = (model["ours_ckpt"]["ms_per_iter"] / model["nccl"]["ms_per_iter"] - 1) * 100
+        model["config"] = (f"GPT-2 small, random init, random tokens, micro-batch {args.micro_batch} x seq 1024 per GPU, "
+                           f"bf16 autocast fwd/bwd (stock PyTorch), DP{world}; ours: CheckmateDDP backward hooks, "
+                           f"tap={args.tap}, persist_every={args.persist_every}")
     cpu = None
     if rank == 0 and world == 1:
         from oracle import oracle as O
@@ -492,7 +507,7 @@ def main():
                        "iters_per_s": res["iters_per_s"]},
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res.get("e2e"),
             "gpu_launches": res["launches"], "clocks": res["clocks"],
-            "nockpt_nccl": base, "nockpt_ours": ours_nockpt,
+            "nockpt_nccl": base, "nockpt_ours": ours_nockpt, "model_mode": model,
             "ckpt_overhead_pct_vs_nccl": overhead,
             "shadow_bit_identical": res["shadow_bit_identical"], "kernels": res["kernels"],
             "host_link_GBps": res["host_link_GBps"],

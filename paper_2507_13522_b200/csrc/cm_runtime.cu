@@ -103,7 +103,11 @@ struct cm_ctx {
     int n = 1, rank = 0, dev = 0, D = 2, dtype = 0, es = 4;
     bool no_tap = false, attach = false, ce_tap = false, no_shadow = false, staged_tap = false;
     void* stage_buf[2] = {};              // default tap: HBM staging of the reduced shard
-    cudaEvent_t ev_stage_free[2] = {};
+    cudaEvent_t ev_stage_free[2] = {};    // staging half drained to the host ring
+    cudaEvent_t ev_ar_done[2] = {};       // all all-reduce kernels of the half's iteration done
+    cudaEvent_t ev_stage_consumed[2] = {};// the shadow step reading the half from HBM is done
+    bool stage_consumer[2] = {false, false};
+    int64_t stage_iter[2] = {-1, -1};     // iteration whose reduced shard the half holds
     int shadow_place = CM_SHADOW_HOST;
     int sms = 148;
     bool cuda_dead = false;
@@ -842,10 +846,19 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
             for (int i = 0; i < 2; ++i) {
                 CU(cudaMalloc(&c->stage_buf[i], (size_t)c->shard_numel * c->es));
                 CU(cudaEventCreateWithFlags(&c->ev_stage_free[i], cudaEventDisableTiming));
+                CU(cudaEventCreateWithFlags(&c->ev_ar_done[i], cudaEventDisableTiming));
+                CU(cudaEventCreateWithFlags(&c->ev_stage_consumed[i], cudaEventDisableTiming));
             }
         }
-        if (c->issued_count == 0)   // staging half t&1 drained (iteration t-2's copies done)
-            CU(cudaStreamWaitEvent(s, c->ev_stage_free[t & 1], 0));
+        if (c->issued_count == 0) {
+            // staging half t&1 held iteration t-2: wait until it is drained to the ring and,
+            // if the shadow step t-1 reads it from HBM, until that step has read it
+            const int h = (int)(t & 1);
+            CU(cudaStreamWaitEvent(s, c->ev_stage_free[h], 0));
+            if (c->stage_consumer[h]) CU(cudaStreamWaitEvent(s, c->ev_stage_consumed[h], 0));
+            c->stage_consumer[h] = false;
+            c->stage_iter[h] = t;
+        }
     }
     if (fused_tap) P.tap = ring_slot_dev(c, slot) + B.shard_off * c->es;
     else if (staged) P.tap = (char*)c->stage_buf[t & 1] + B.shard_off * c->es;
@@ -888,7 +901,10 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     if (!c->no_tap && c->issued_count == (int)c->buckets.size()) {
         const bool via_ce = c->ce_tap || staged;
         CU(cudaEventRecord(c->ev_tap_done[slot], via_ce ? c->cs_tap : s));
-        if (staged) CU(cudaEventRecord(c->ev_stage_free[t & 1], c->cs_tap));
+        if (staged) {
+            CU(cudaEventRecord(c->ev_stage_free[t & 1], c->cs_tap));
+            CU(cudaEventRecord(c->ev_ar_done[t & 1], s));
+        }
     }
     return CM_OK;
 }
@@ -962,7 +978,7 @@ static cm_status ensure_staging(cm_ctx* c) {
 // gradients since it -- every step remains recoverable from host memory alone (restore
 // rolls forward over the ring), with 12/K instead of 12 bytes per element of D2H.
 static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars& a, cudaStream_t s,
-                                     bool force_persist, bool* persisted) {
+                                     bool force_persist, bool* persisted, const char* dev_g = nullptr) {
     const int slot = (int)((step - 1) % c->D);
     const int hin = (int)((step - 1) & 1), hout = (int)(step & 1);
     cm_status st = ensure_staging(c);
@@ -986,16 +1002,18 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars&
         for (int64_t lo = 0, i = 0; lo < L; lo += C, ++i) {
             const int j = (int)(i % kStages);
             const int64_t len = std::min(C, L - lo);
-            // copy engine H2D of the ring chunk into staging j (once the kernel that used
-            // staging j kStages chunks ago is done)
-            CU(cudaStreamWaitEvent(c->cs_h2d, c->ev_stg_free[j], 0));
-            CU(cudaMemcpyAsync(c->stg_g[j], ring + lo * c->es, (size_t)len * c->es, cudaMemcpyHostToDevice,
-                               c->cs_h2d));
-            CU(cudaEventRecord(c->ev_stg_ready[j], c->cs_h2d));
-            // AdamW on its own stream: a kernel delayed by busy SMs does not stall the copies
-            CU(cudaStreamWaitEvent(c->cs_k, c->ev_stg_ready[j], 0));
+            if (!dev_g) {
+                // copy engine H2D of the ring chunk into staging j (once the kernel that used
+                // staging j kStages chunks ago is done)
+                CU(cudaStreamWaitEvent(c->cs_h2d, c->ev_stg_free[j], 0));
+                CU(cudaMemcpyAsync(c->stg_g[j], ring + lo * c->es, (size_t)len * c->es, cudaMemcpyHostToDevice,
+                                   c->cs_h2d));
+                CU(cudaEventRecord(c->ev_stg_ready[j], c->cs_h2d));
+                // AdamW on its own stream: a kernel delayed by busy SMs does not stall the copies
+                CU(cudaStreamWaitEvent(c->cs_k, c->ev_stg_ready[j], 0));
+            }
             AdamParams P{};
-            P.g = c->stg_g[j];
+            P.g = dev_g ? (const void*)(dev_g + lo * c->es) : (const void*)c->stg_g[j];
             P.n = len;
             P.s = a;
             P.p_in = c->sd[hin][0] + lo; P.m_in = c->sd[hin][1] + lo; P.v_in = c->sd[hin][2] + lo;
@@ -1037,10 +1055,22 @@ cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
     if (c->train_step < step || c->slot_sc_step[slot] != step)
         return fail(c, CM_ERR_STATE, "shadow step %lld before cm_apply_step(%lld)", (long long)step, (long long)step);
     cudaStream_t s = S(side_stream);
-    CU(cudaStreamWaitEvent(s, c->ev_tap_done[slot], 0));   // all taps of iteration step-1
+    // the shadow reads iteration step-1's reduced gradients from the HBM staging half the
+    // tap wrote (no host-link traffic), unless that half was already reused (the shadow fell
+    // more than one iteration behind): then from the host ring (copy-engine H2D)
+    const int64_t it = step - 1;
+    const int h = (int)(it & 1);
+    const bool from_stage = c->staged_tap && c->stage_buf[h] && c->stage_iter[h] == it;
+    if (from_stage) CU(cudaStreamWaitEvent(s, c->ev_ar_done[h], 0));
+    else CU(cudaStreamWaitEvent(s, c->ev_tap_done[slot], 0));   // all taps of iteration step-1
     bool persisted = false;
-    cm_status st = shadow_step_enqueue(c, step, c->slot_sc[slot], s, false, &persisted);
+    cm_status st = shadow_step_enqueue(c, step, c->slot_sc[slot], s, false, &persisted,
+                                       from_stage ? (const char*)c->stage_buf[h] : nullptr);
     if (st != CM_OK) return st;
+    if (from_stage) {
+        CU(cudaEventRecord(c->ev_stage_consumed[h], s));
+        c->stage_consumer[h] = true;
+    }
     // release ring slots: DEVICE placement once consumed; HOST placement once a persisted
     // snapshot covers them (the ring is the log that makes every step recoverable)
     if (c->shadow_place == CM_SHADOW_DEVICE || persisted) {
@@ -1272,6 +1302,8 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     c->train_step = I;
     c->shadow_enq = I;
     c->released_upto = I;   // step I is persisted (HOST) / held in HBM (DEVICE)
+    c->stage_iter[0] = c->stage_iter[1] = -1;   // staging halves hold nothing of the new run
+    c->stage_consumer[0] = c->stage_consumer[1] = false;
     for (int i = 0; i < c->D; ++i) c->slot_sc_step[i] = -1;
     *restored = I;
     return CM_OK;
@@ -1346,6 +1378,8 @@ cm_status cm_finalize(cm_ctx* c) {
     for (int i = 0; i < 2; ++i) {
         if (c->stage_buf[i]) cudaFree(c->stage_buf[i]);
         if (c->ev_stage_free[i]) cudaEventDestroy(c->ev_stage_free[i]);
+        if (c->ev_ar_done[i]) cudaEventDestroy(c->ev_ar_done[i]);
+        if (c->ev_stage_consumed[i]) cudaEventDestroy(c->ev_stage_consumed[i]);
     }
     if (c->ev_ar) cudaEventDestroy(c->ev_ar);
     if (c->stg_ready) {

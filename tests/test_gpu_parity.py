@@ -465,3 +465,27 @@ def test_consolidation_min_rule_across_lagging_shards():
             assert r.ctx.verify(g.stream) == -1
     finally:
         close(g)
+
+
+def test_lagging_shadow_falls_back_from_staging_to_ring():
+    """The shadow normally reads the reduced shard from the tap's HBM staging half; when it
+    lags so far that the half was reused, it reads the host ring instead.  Both bit-exact."""
+    numel = TABLES["ragged"]
+    n = 2
+    g = make_group(numel, n, D=4)
+    plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
+    try:
+        for _ in range(3):
+            g.step(shadow=False)        # iterations 0,1,2: staging half 0 now holds iteration 2
+            ref.step()
+        g.shadow(step=1)                # iteration 0: staging reused -> host ring
+        g.shadow(step=2)                # iteration 1: staging half 1
+        g.shadow(step=3)                # iteration 2: staging half 0
+        g.sync()
+        for r in g.ranks:
+            assert r.ctx.verify(g.stream) == -1
+        sp, sm, sv = shadow_flat(g, 3 & 1)
+        np.testing.assert_array_equal(bits(sp), bits(ref.sp))
+        np.testing.assert_array_equal(bits(sv), bits(ref.sv))
+    finally:
+        close(g)

@@ -19,6 +19,8 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+from paper_2507_13522_b200.modelbench import run_arm  # noqa: E402
+
 
 def setup():
     if "RANK" not in os.environ:
@@ -31,81 +33,6 @@ def setup():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return dist.get_rank(), dist.get_world_size(), local
-
-
-def make_model(seed):
-    from transformers import GPT2Config, GPT2LMHeadModel
-    torch.manual_seed(seed)
-    cfg = GPT2Config()
-    cfg._attn_implementation = "sdpa"
-    return GPT2LMHeadModel(cfg)
-
-
-def run_arm(arm, args, rank, world, local):
-    from paper_2507_13522_b200 import cm
-    from paper_2507_13522_b200.ddp import CheckmateDDP
-    dev = torch.device("cuda", local)
-    model = make_model(0).to(dev)
-    model.train()
-    g = torch.Generator(device=dev)
-    g.manual_seed(1000 + rank)
-    tokens = torch.randint(0, 50257, (args.steps + args.warmup, args.micro_batch, 1024), device=dev, generator=g)
-    if arm == "nccl":
-        ddp = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local], bucket_cap_mb=25,
-                                                        gradient_as_bucket_view=True)
-        opt = torch.optim.AdamW(model.parameters(), lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01,
-                                fused=True)
-
-        def it(i):
-            opt.zero_grad(set_to_none=False)
-            with torch.autocast("cuda", dtype=torch.bfloat16):
-                loss = ddp(tokens[i], labels=tokens[i]).loss
-            loss.backward()
-            opt.step()
-        streams = []
-        cleanup = lambda: None   # noqa: E731
-    else:
-        flags = cm.CM_FLAG_NO_TAP if arm == "ours_nockpt" else (
-            {"ce": cm.CM_FLAG_TAP_COPYENGINE, "direct": cm.CM_FLAG_TAP_DIRECT}.get(args.tap, 0))
-        if arm == "ours_tap_only":                  # tap into the ring, no shadow replica
-            flags |= cm.CM_FLAG_NO_SHADOW
-        name = f"cmmm_{os.environ.get('MASTER_PORT', '0')}_{arm}"
-        cd = CheckmateDDP(model, local, world, rank, shm_name=name, ring_depth=args.ring_depth,
-                          persist_every=args.persist_every, flags=flags)
-
-        def it(i):
-            cd.zero_grad()
-            with torch.autocast("cuda", dtype=torch.bfloat16):
-                loss = model(tokens[i], labels=tokens[i]).loss
-            loss.backward()
-            cd.step()
-        streams = [cd.comm, cd.side]
-
-        def cleanup():
-            full = not (flags & (cm.CM_FLAG_NO_TAP | cm.CM_FLAG_NO_SHADOW))
-            ok = cd.r.ctx.verify(torch.cuda.current_stream()) == -1 if full else None
-            cd.finalize()
-            cm.unlink_shadow(name, rank)
-            return ok
-    for i in range(args.warmup):
-        it(i)
-    torch.cuda.synchronize()
-    dist.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    cur = torch.cuda.current_stream()
-    a.record(cur)
-    for i in range(args.warmup, args.warmup + args.steps):
-        it(i)
-    for s in streams:
-        cur.wait_stream(s)
-    b.record(cur)
-    b.synchronize()
-    ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ok = cleanup()
-    del model
-    torch.cuda.empty_cache()
-    return {"ms_per_iter": ms.item(), "shadow_bit_identical": ok}
 
 
 def main():

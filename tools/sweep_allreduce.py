@@ -25,7 +25,7 @@ from paper_2507_13522_b200 import cm, harness  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", default="ours_tap", choices=["ours_tap", "ours", "nccl"])
+    ap.add_argument("--mode", default="ours_tap", choices=["ours_tap", "ours_tap_direct", "ours", "nccl"])
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--min-mib", type=int, default=1)
     ap.add_argument("--max-mib", type=int, default=1024)
@@ -50,7 +50,8 @@ def main():
             fn = lambda t: dist.all_reduce(buf)   # noqa: E731
             ctx = None
         else:
-            flags = cm.CM_FLAG_NO_SHADOW if args.mode == "ours_tap" else cm.CM_FLAG_NO_TAP
+            flags = {"ours_tap": cm.CM_FLAG_NO_SHADOW, "ours": cm.CM_FLAG_NO_TAP,
+                     "ours_tap_direct": cm.CM_FLAG_NO_SHADOW | cm.CM_FLAG_TAP_DIRECT}[args.mode]
             name = f"cmsw_{os.environ.get('MASTER_PORT', '0')}_{mib}"
             R = harness.DistRank(numel, dtype, S + 1, name, 2, cm.CM_SHADOW_HOST, flags)
             if args.ar_blocks:
@@ -80,7 +81,7 @@ def main():
                               "dtype": args.dtype, "n": n, "bytes": S, "ms": med,
                               "p10_ms": sorted(times)[len(times) // 10], "p90_ms": sorted(times)[9 * len(times) // 10],
                               "algbw_GBps": S / sec / 1e9, "busbw_GBps": 2 * (n - 1) / n * S / sec / 1e9,
-                              "tap_GBps_per_gpu": (S / n) / sec / 1e9 if args.mode == "ours_tap" else 0.0}),
+                              "tap_GBps_per_gpu": (S / n) / sec / 1e9 if args.mode.startswith("ours_tap") else 0.0}),
                   flush=True)
         if ctx is not None:
             dist.barrier()
