@@ -185,7 +185,7 @@ def traffic_table():
         return {}
 
 
-def time_steps(step_fn, streams, k):
+def time_steps(step_fn, streams, k, ctx=None):
     import torch
     s0 = streams[0]
     a = torch.cuda.Event(enable_timing=True)
@@ -193,10 +193,12 @@ def time_steps(step_fn, streams, k):
     a.record(s0)
     for _ in range(k):
         step_fn()
-    for s in streams[1:]:                      # the shadow's drain counts (conservative)
+    for s in streams[1:]:                      # the shadow's work counts (conservative)
         e = torch.cuda.Event()
         e.record(s)
         s0.wait_event(e)
+    if ctx is not None:                        # and so do the library's tap drains/persists
+        ctx.join(s0)
     b.record(s0)
     b.synchronize()
     return a.elapsed_time(b)
@@ -231,7 +233,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     launches0 = ctx.info().launches
     ctx.timing(True)
     with ClockSampler(local) as clk:
-        ms = time_steps(step, [R.stream, R.side], args.steps)
+        ms = time_steps(step, [R.stream, R.side], args.steps, ctx)
     kms, kcnt = ctx.timing(False)
     launches = ctx.info().launches - launches0
     ms_max = max_over_ranks(ms)
@@ -240,70 +242,70 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     # bit-identity of the shadow after the timed run (verify synchronises)
     mismatch = ctx.verify(R.stream)
 
-    # ----- per-kernel roofline (average launch duration, live events on each kernel's stream)
+    # ----- per-kernel rooflines (average launch duration, live events on each kernel's stream)
+    # and the step's binding resource.  Algorithmic bytes per unit are in DESIGN.md 6.
     n = world
     hbm_peak, hbm_src = measured_peaks()
     link = host_link_peaks(dev)
     nb = info.n_buckets
+    P = info.padded_numel
+    L = info.shard_numel
+    K = max(1, args.persist_every) if place == cm.CM_SHADOW_HOST else 1
     kern = {}
     ar_ms = kms[0] / max(kcnt[0], 1)
-    ar_bytes_nvl = 2.0 * (n - 1) / n * S_bytes / nb                  # per launch, per GPU, both directions
-    ar_bytes_tap = S_bytes / n / nb
-    kern["rs_tap_ag"] = {"avg_ms": ar_ms, "launches": kcnt[0],
-                         "nvlink_GBps_per_dir": (ar_bytes_nvl / 2) / (ar_ms * 1e-3) / 1e9 if n > 1 else 0.0,
-                         "tap_GBps": ar_bytes_tap / (ar_ms * 1e-3) / 1e9,
-                         "share": kms[0] / ms}
+    Sb = S_bytes / nb                                            # average bucket bytes
+    ar_nvl = (n - 1) / n * Sb                                    # per direction, per GPU
+    ar_hbm = 2 * Sb + (Sb / n if args.tap == "staged" else 0)    # local + peers' reads/writes (+ staging)
+    if n == 1:
+        ar_hbm = (2 * Sb) if args.tap == "staged" else Sb        # copy to staging / read for a direct tap
+    ent = {"avg_ms": ar_ms, "launches": kcnt[0], "share": kms[0] / ms}
+    if n > 1:
+        ent.update(bound="nvlink", achieved=ar_nvl / (ar_ms * 1e-3) / 1e9, peak=NVLINK_PEAK_GBS, unit="GB/s",
+                   bytes_per_launch=ar_nvl, peak_source="B200_PROFILING.md measured peer copy, per direction")
+    elif args.tap == "direct":
+        ent.update(bound="host_link", achieved=(Sb) / (ar_ms * 1e-3) / 1e9, peak=link["d2h"], unit="GB/s",
+                   bytes_per_launch=Sb, peak_source="measured pinned D2H copy (this run)")
+    else:
+        ent.update(bound="hbm", achieved=ar_hbm / (ar_ms * 1e-3) / 1e9, peak=hbm_peak, unit="GB/s",
+                   bytes_per_launch=ar_hbm, peak_source=hbm_src)
+    ent["frac"] = ent["achieved"] / ent["peak"]
+    kern["rs_tap_ag"] = ent
     ad_ms = kms[1] / max(kcnt[1], 1)
-    ad_bytes = info.padded_numel * (es + 24)
-    kern["adamw_step"] = {"avg_ms": ad_ms, "launches": kcnt[1], "hbm_GBps": ad_bytes / (ad_ms * 1e-3) / 1e9,
-                          "hbm_frac": ad_bytes / (ad_ms * 1e-3) / 1e9 / hbm_peak, "share": kms[1] / ms}
+    ad_bytes = P * (es + 24)
+    kern["adamw_step"] = {"avg_ms": ad_ms, "launches": kcnt[1], "share": kms[1] / ms, "bound": "hbm",
+                          "achieved": ad_bytes / (ad_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                          "bytes_per_launch": ad_bytes, "peak_source": hbm_src}
+    kern["adamw_step"]["frac"] = kern["adamw_step"]["achieved"] / hbm_peak
     sh_ms = kms[2] / max(kcnt[2], 1)
-    # shadow step (copy-engine staged): H2D = ring grads; D2H = new p/m/v persisted (HOST)
-    sh_h2d = info.shard_numel * es
-    K = max(1, args.persist_every) if place == cm.CM_SHADOW_HOST else 1
-    sh_d2h = info.shard_numel * (12 if place == cm.CM_SHADOW_HOST else 0) / K   # per step (avg)
-    kern["shadow_step"] = {"avg_ms": sh_ms, "launches": kcnt[2], "h2d_GBps": sh_h2d / (sh_ms * 1e-3) / 1e9,
-                           "d2h_GBps": sh_d2h / (sh_ms * 1e-3) / 1e9, "share": kms[2] / ms,
-                           "what": "H2D ring chunk -> HBM AdamW (ping-pong halves) -> D2H persist, pipelined"}
+    sh_hbm = L * (es + 24)
+    sh_d2h = L * 12 / K if place == cm.CM_SHADOW_HOST else 0.0
+    kern["shadow_step"] = {"avg_ms": sh_ms, "launches": kcnt[2], "share": kms[2] / ms,
+                           "hbm_bytes": sh_hbm, "d2h_bytes_avg": sh_d2h,
+                           "what": "AdamW on the shard from the tap's HBM staging (host-ring fallback), "
+                                   "persist to the host snapshot every K steps (copy engine)"}
     gen_ms = kms[3] / max(kcnt[3], 1)
     kern["gen_grads"] = {"avg_ms": gen_ms, "launches": kcnt[3], "share": kms[3] / ms}
-
-    # dominant kernel -> roofline object
-    shares = {k: v["share"] for k, v in kern.items()}
-    dom = max(shares, key=shares.get)
-    traf = traffic_table()
-    if dom == "adamw_step":
-        roof = {"kernel": dom, "bound": "hbm", "achieved": kern[dom]["hbm_GBps"], "peak": hbm_peak,
-                "unit": "GB/s", "peak_source": hbm_src, "bytes_per_launch": ad_bytes}
-    elif dom == "shadow_step":
-        if sh_d2h > 0:
-            roof = {"kernel": dom, "bound": "host_link", "achieved": kern[dom]["d2h_GBps"], "peak": link["d2h"],
-                    "unit": "GB/s", "peak_source": "measured pinned D2H copy (this run)",
-                    "bytes_per_launch": sh_d2h, "direction": "d2h"}
-        else:
-            roof = {"kernel": dom, "bound": "host_link", "achieved": kern[dom]["h2d_GBps"], "peak": link["h2d"],
-                    "unit": "GB/s", "peak_source": "measured pinned H2D copy (this run)",
-                    "bytes_per_launch": sh_h2d, "direction": "h2d"}
-    elif dom == "rs_tap_ag":
-        t_nvl = (ar_bytes_nvl / 2) / (NVLINK_PEAK_GBS * 1e9) if n > 1 else 0.0
-        t_tap = ar_bytes_tap / (link["d2h"] * 1e9)
-        if t_nvl >= t_tap:
-            roof = {"kernel": dom, "bound": "nvlink", "achieved": kern[dom]["nvlink_GBps_per_dir"],
-                    "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "peak_source": "B200_PROFILING.md measured peer copy",
-                    "bytes_per_launch": ar_bytes_nvl / 2}
-        else:
-            roof = {"kernel": dom, "bound": "host_link", "achieved": kern[dom]["tap_GBps"], "peak": link["d2h"],
-                    "unit": "GB/s", "peak_source": "measured pinned D2H copy (this run)",
-                    "bytes_per_launch": ar_bytes_tap, "direction": "d2h"}
-    else:
-        roof = {"kernel": dom, "bound": "alu", "achieved": None, "peak": None, "unit": None}
-    if roof.get("achieved") is not None:
-        roof["frac"] = roof["achieved"] / roof["peak"]
-    # the whole step's use of the host link (tap + persisted shadow state share D2H)
+    traf = traffic_table().get(f"{args.workload}_n{n}_{args.shadow}", {})
+    for k in kern:
+        if k in traf:
+            kern[k]["traffic"] = traf[k].get("dram_bytes_per_launch")
+    # the step's binding resource: the host link carries the tap (S/n per GPU) and the
+    # persisted shadow state (12 L / K); our kernels each run near their own roofs
     step_d2h = S_bytes / n + sh_d2h
-    roof["step_host_link_d2h"] = {"bytes_per_step": step_d2h, "GBps": step_d2h / (ms_step * 1e-3) / 1e9,
-                                  "frac": step_d2h / (ms_step * 1e-3) / 1e9 / link["d2h"]}
-    roof["traffic"] = traf.get(f"{args.workload}_n{n}_{args.shadow}", {}).get(dom)
+    t_link = step_d2h / (link["d2h"] * 1e9)
+    t_kern = max(kms[0], kms[1]) / args.steps * 1e-3
+    if t_link >= t_kern:
+        roof = {"kernel": "tap drain + shadow persist (copy engines, host link D2H)", "bound": "host_link",
+                "achieved": step_d2h / (ms_step * 1e-3) / 1e9, "peak": link["d2h"], "unit": "GB/s",
+                "bytes_per_step": step_d2h, "peak_source": "measured pinned D2H copy (this run)",
+                "note": "the checkpointed step in synthetic mode (no compute to hide under) is bound by the "
+                        "host link; per-kernel rooflines are in 'kernels'"}
+    else:
+        dk = "rs_tap_ag" if kms[0] >= kms[1] else "adamw_step"
+        roof = {"kernel": dk, **{k: kern[dk][k] for k in ("bound", "achieved", "peak", "unit", "bytes_per_launch",
+                                                           "peak_source")}}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = traf.get(roof["kernel"], {}).get("dram_bytes_per_launch") if roof["kernel"] in traf else None
 
     result = {"ms_step": ms_step, "iters_per_s": iters_per_s, "launches": launches, "kernels": kern,
               "roofline": roof, "clocks": clk.summary(), "shadow_bit_identical": mismatch == -1,
@@ -353,7 +355,7 @@ def run_e2e(args, R, S_bytes, es):
         step()
     R.sync()
     k = max(3, args.steps // 2)
-    ms = time_steps(step, [R.stream, R.side], k)
+    ms = time_steps(step, [R.stream, R.side], k, c)
     ms = max_over_ranks(ms)
     return {"value": 1000.0 / (ms / k) * R.n, "unit": UNIT, "h2d_bytes_per_step": S_bytes,
             "d2h_bytes_per_step": 8, "ms_per_step": ms / k,

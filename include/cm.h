@@ -241,6 +241,11 @@ cm_status cm_bucket_info(const cm_ctx *ctx, int32_t bucket, int64_t *elem_off, i
 /* Host pointers into the shadow: state half h (0/1) as shard-local arrays of
  * shard_numel fp32 (HOST placement only; DEVICE placement returns device pointers),
  * and ring slot k (shard-local, grad dtype).  For tests and tools.                     */
+/* cm_join -- make `stream` wait for everything the library has enqueued on its internal
+ * streams so far (copy-engine tap drains to the host ring, shadow staging/persist copies).
+ * Stream-ordered, no host synchronisation.  Benchmarks call it before stopping a timer.   */
+cm_status cm_join(cm_ctx *ctx, void *stream);
+
 /* cm_set_param -- tuning knobs used by benchmarks and ablations (defaults are the
  * measured best); CM_ERR_ARG for an unknown key or out-of-range value.
  *   "adamw_impl"          AdamW data movement (same arithmetic): 0 per-thread 128-bit items,

@@ -26,7 +26,7 @@ CM_FLAG_TAP_DIRECT = 1 << 4     # default tap is "staged" (HBM staging + copy-en
 EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
            "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step",
            "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_get_info",
-           "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_set_param"]
+           "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_set_param", "cm_join"]
 
 
 class cm_config(C.Structure):
@@ -92,6 +92,7 @@ def lib():
         L.cm_shadow_view.argtypes = [P, C.c_int32, C.POINTER(P), C.POINTER(P), C.POINTER(P)]
         L.cm_ring_view.argtypes = [P, C.c_int32, C.POINTER(P)]
         L.cm_set_param.argtypes = [P, C.c_char_p, C.c_int64]
+        L.cm_join.argtypes = [P, P]
         L.cm_timing.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         for name in EXPORTS:
             if name not in ("cm_blob_size", "cm_last_error"):
@@ -215,6 +216,9 @@ class Context:
         g = C.c_void_p()
         self._check(lib().cm_ring_view(self._ctx, int(slot), C.byref(g)))
         return g.value
+
+    def join(self, stream=None):
+        self._check(lib().cm_join(self._ctx, _stream_ptr(stream)))
 
     def set_param(self, key, value):
         self._check(lib().cm_set_param(self._ctx, key.encode(), int(value)))

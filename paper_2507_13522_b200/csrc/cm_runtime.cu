@@ -410,6 +410,22 @@ struct TimedScope {
 // ====================================================================== C ABI
 extern "C" {
 
+cm_status cm_join(cm_ctx* c, void* stream) {
+    if (!c) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    cudaStream_t s = S(stream);
+    cudaStream_t internal[4] = {c->cs_tap, c->cs_h2d, c->cs_d2h, c->cs_k};
+    for (cudaStream_t q : internal) {
+        if (!q) continue;
+        cudaEvent_t e;
+        CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CU(cudaEventRecord(e, q));
+        CU(cudaStreamWaitEvent(s, e, 0));
+        CU(cudaEventDestroy(e));
+    }
+    return CM_OK;
+}
+
 cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     if (!c || !key) return CM_ERR_ARG;
     const std::string k = key;
