@@ -1014,7 +1014,10 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars&
         CU(cudaStreamWaitEvent(c->cs_h2d, c->ev_fork, 0));
         CU(cudaStreamWaitEvent(c->cs_k, c->ev_fork, 0));
         CU(cudaStreamWaitEvent(c->cs_d2h, c->ev_fork, 0));
-        const int64_t L = c->shard_numel, C = c->stg_elems;
+        // chunks pipeline the H2D (ring fallback) or the D2H persist with the kernels; with
+        // the gradients already in HBM and nothing to persist, one launch covers the shard
+        const int64_t L = c->shard_numel;
+        const int64_t C = (dev_g && !persist) ? std::max<int64_t>(L, 1) : c->stg_elems;
         for (int64_t lo = 0, i = 0; lo < L; lo += C, ++i) {
             const int j = (int)(i % kStages);
             const int64_t len = std::min(C, L - lo);
