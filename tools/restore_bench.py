@@ -1,0 +1,86 @@
+"""C5 failure/restore at GPT-2 scale: kill every rank at iteration k (no cleanup: the
+processes exit, only the host shadow segments survive), relaunch, attach, restore from the
+shadow, continue 100 iterations, and compare sampled elements of every rank's state with
+the oracle's uninterrupted trajectories, bit for bit.
+
+  python -m torch.distributed.run --nproc-per-node N tools/restore_bench.py phase1 <name> [k]
+  python -m torch.distributed.run --nproc-per-node N tools/restore_bench.py phase2 <name> [k] [more]
+Rank 0 of phase 2 prints one JSON line (restore wall time, restored step, bit-exactness).
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2507_13522_b200 import cm, harness  # noqa: E402
+from paper_2507_13522_b200 import workloads as W  # noqa: E402
+
+
+def main():
+    phase, name = sys.argv[1], sys.argv[2]
+    k = int(sys.argv[3]) if len(sys.argv) > 3 else 7
+    more = int(sys.argv[4]) if len(sys.argv) > 4 else 100
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, n = dist.get_rank(), dist.get_world_size()
+    numel = W.numels(W.gpt2_small())
+    flags = cm.CM_FLAG_ATTACH if phase == "phase2" else 0
+    R = harness.DistRank(numel, cm.CM_F32, W.CAP_BYTES, name, 16, cm.CM_SHADOW_HOST, flags, persist_every=8)
+    if phase == "phase1":
+        for _ in range(k):
+            R.step()
+        # die with work still in flight (no stream sync, no finalize): whatever the GPUs did
+        # not finish is lost; only the host shadow segments in /dev/shm survive
+        dist.barrier()
+        os._exit(0)
+    # phase 2: fresh processes, garbage training state
+    R.r.p.fill_(float("nan"))
+    R.r.m.fill_(float("nan"))
+    R.r.v.fill_(float("nan"))
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    I = R.r.ctx.restore(R.stream)
+    torch.cuda.synchronize()
+    restore_s = time.perf_counter() - t0
+    R.t = I
+    for _ in range(more):
+        R.step()
+    R.sync()
+    ok_shadow = R.r.ctx.verify(R.stream) == -1
+    # sampled bitwise comparison with the oracle's uninterrupted trajectories
+    from oracle import oracle as O
+    plan = O.Plan(numel, W.CAP_BYTES, 4, n)
+    rng = np.random.default_rng(rank)
+    idx = np.sort(rng.choice(plan.total, 1 << 14, replace=False)).astype(np.int64)
+    used = np.ones(len(idx), np.uint8)        # GPT-2 needs no padding at n <= 8
+    p, m, v, Rl = O.run_sample(W.SEED, n, O.F32, W.GRAD_SCALE, I + more, idx, used, lr=W.HP["lr"],
+                               b1=W.HP["beta1"], b2=W.HP["beta2"], eps=W.HP["eps"], wd=W.HP["weight_decay"])
+    ti = torch.from_numpy(idx).to(R.r.p.device)
+    same = all(np.array_equal(a[ti].cpu().numpy().view(np.uint32), b.view(np.uint32))
+               for a, b in ((R.r.p, p), (R.r.m, m), (R.r.v, v)))
+    res = torch.tensor([restore_s, float(same and ok_shadow)], dtype=torch.float64, device=R.r.p.device)
+    dist.all_reduce(res, op=dist.ReduceOp.MAX)
+    ok_all = torch.tensor([float(same and ok_shadow)], dtype=torch.float64, device=R.r.p.device)
+    dist.all_reduce(ok_all, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps({"n": n, "killed_after_iterations": k, "restored_step": I, "restore_s_max_over_ranks": res[0].item(),
+                          "continued_iterations": more, "bit_exact_vs_oracle_and_shadow": bool(ok_all.item() == 1.0),
+                          "sampled_elements_per_rank": int(len(idx)), "persist_every": 8, "ring_depth": 16}),
+              flush=True)
+    dist.barrier()
+    R.r.ctx.finalize()
+    cm.unlink_shadow(name, rank)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
