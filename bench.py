@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-baseline", action="store_true", help="skip the NCCL + torch fused AdamW arm")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="target seconds of oracle work")
+    ap.add_argument("--zero1", action="store_true",
+                    help="sharded AdamW state: reduce-scatter + tap, AdamW on the own shard fused with the "
+                         "NVLink all-gather of the updated parameters (SURVEY 8 f3)")
     ap.add_argument("--no-model", action="store_true",
                     help="skip the GPT-2 model-mode arms (real fwd/bwd; checkpoint overhead vs NCCL DDP)")
     ap.add_argument("--model-steps", type=int, default=10)
@@ -216,6 +219,8 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     if world > 1:
         shm = f"cmbench_{os.environ.get('MASTER_PORT', '0')}"
     flags = {"ce": cm.CM_FLAG_TAP_COPYENGINE, "direct": cm.CM_FLAG_TAP_DIRECT}.get(args.tap, 0)
+    if args.zero1:
+        flags |= cm.CM_FLAG_ZERO1
     R = harness.DistRank(numel, dtype, cap, shm, args.ring_depth, place, flags, persist_every=args.persist_every)
     ctx = R.r.ctx
     info = ctx.info()
@@ -408,7 +413,8 @@ def run_ours_nockpt(args, rank, world, local, numel, dtype, cap):
     import torch
     import torch.distributed as dist
     from paper_2507_13522_b200 import cm, harness
-    R = harness.DistRank(numel, dtype, cap, "unused", 2, cm.CM_SHADOW_HOST, cm.CM_FLAG_NO_TAP)
+    R = harness.DistRank(numel, dtype, cap, "unused", 2, cm.CM_SHADOW_HOST,
+                         cm.CM_FLAG_NO_TAP | (cm.CM_FLAG_ZERO1 if args.zero1 else 0))
     for _ in range(args.warmup):
         R.step()
     R.sync()
@@ -485,7 +491,8 @@ def main():
         import types
         from paper_2507_13522_b200.modelbench import run_arm
         margs = types.SimpleNamespace(steps=args.model_steps, warmup=max(3, args.warmup), micro_batch=args.micro_batch,
-                                      ring_depth=args.ring_depth, persist_every=args.persist_every, tap=args.tap)
+                                      ring_depth=args.ring_depth, persist_every=args.persist_every, tap=args.tap,
+                                      zero1=args.zero1)
         model = {arm: run_arm(arm, margs, rank, world, local) for arm in ("nccl", "ours_nockpt", "ours_ckpt")}
         model["ckpt_overhead_pct_vs_nccl"] = (model["ours_ckpt"]["ms_per_iter"] / model["nccl"]["ms_per_iter"] - 1) * 100
         model["config"] = (f"GPT-2 small, random init, random tokens, micro-batch {args.micro_batch} x seq 1024 per GPU, "
@@ -504,7 +511,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if dtype == cm.CM_F32 else "bf16-grads/f32-state", "data": "synthetic",
             "config": {"workload": name, "ranks": world, "shadow": args.shadow, "ring_depth": args.ring_depth,
-                       "tap": args.tap, "persist_every": args.persist_every,
+                       "tap": args.tap, "persist_every": args.persist_every, "zero1": args.zero1,
                        "parallelism": f"dp{world}", "l2": "inputs larger than L2 (working set >> 126 MB)",
                        "iters_per_s": res["iters_per_s"]},
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res.get("e2e"),

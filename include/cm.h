@@ -78,6 +78,14 @@ typedef enum { CM_SHADOW_HOST = 0, CM_SHADOW_DEVICE = 1 } cm_shadow_place;
 #define CM_FLAG_TAP_DIRECT (1ull << 4) /* the kernel stores the reduced registers straight into
                                          the pinned host ring (zero extra HBM traffic; the
                                          kernel then runs at host-link speed)               */
+#define CM_FLAG_ZERO1 (1ull << 5)      /* sharded optimizer state (ZeRO-1, SURVEY 8 row f3,
+                                         PAPER.md:670-674): the kernel reduce-scatters (no
+                                         gradient all-gather); cm_apply_step runs AdamW on
+                                         this rank's shard only and all-gathers the updated
+                                         parameters over NVLink in the same kernel.  m and v
+                                         passed to cm_register_buckets are then shard-local
+                                         arrays of P_pad/n elements.  Bit-identical to the
+                                         unsharded path (same element arithmetic).         */
 #define CM_FLAG_NO_SHADOW (1ull << 3) /* benchmark mode (bucket sweep): tap into the ring but
                                          keep no shadow replica and no flow control; the ring
                                          is overwritten freely; shadow/verify/restore refuse */
@@ -139,6 +147,8 @@ cm_status cm_init(const cm_config *cfg, cm_ctx **out);
  *   grad   device, P_pad elements of grad_dtype: this rank's gradients in the flat
  *          layout; after cm_allreduce_multicast of bucket b it holds the reduced SUM.
  *   p,m,v  device, P_pad fp32 each: master weights and AdamW moments (flat layout).
+ *          With CM_FLAG_ZERO1, m and v hold P_pad/n elements: this rank's shard, in the
+ *          shard-local order (shard r of bucket b at offset off_b/n).
  * All four must be 16-byte aligned, must outlive the context, and are owned by the
  * caller.  Writes an opaque exchange blob (this rank's IPC handles) into blob_out; on
  * entry *blob_len is its capacity (cm_blob_size() bytes suffice), on exit its length.

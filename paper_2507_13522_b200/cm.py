@@ -20,6 +20,7 @@ CM_FLAG_NO_TAP = 1 << 0
 CM_FLAG_ATTACH = 1 << 1
 CM_FLAG_TAP_COPYENGINE = 1 << 2
 CM_FLAG_NO_SHADOW = 1 << 3
+CM_FLAG_ZERO1 = 1 << 5          # sharded AdamW state + fused parameter all-gather
 CM_FLAG_TAP_DIRECT = 1 << 4     # default tap is "staged" (HBM staging + copy-engine drain)
 
 # every symbol include/cm.h declares (tests check the library exports all of them)

@@ -179,8 +179,10 @@ __global__ void __launch_bounds__(256) init_state_kernel(float* __restrict__ p, 
         for (int k = 0; k < 4; ++k)
             w[k] = (i0 + k < lim) ? __float_as_uint(__fmul_rn(gen_f32(K, (uint64_t)(i0 + k), 0), 0.03125f)) : 0u;
         st_v4(p + i0, make_uint4(w[0], w[1], w[2], w[3]));
-        st_v4(m + i0, make_uint4(0, 0, 0, 0));
-        st_v4(v + i0, make_uint4(0, 0, 0, 0));
+        if (m) {   // (ZeRO-1: m, v are shard-local and zeroed separately)
+            st_v4(m + i0, make_uint4(0, 0, 0, 0));
+            st_v4(v + i0, make_uint4(0, 0, 0, 0));
+        }
     }
 }
 
@@ -599,6 +601,69 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adamw_tma_kernel(const AdamPar
     }
 }
 
+// ------------------------------------------------------------------ ZeRO-1: AdamW + AG
+// SURVEY 8 row f3 (PAPER.md:670-674 discusses sharded optimizers): after the reduce-scatter
+// rank r owns the reduced shard r of every bucket (in the tap's HBM staging half).  It
+// applies the same AdamW (adamw_elem: identical bits) to its shard only -- m, v are
+// shard-local arrays -- and stores each updated parameter once into its own p and once
+// into every peer's p over NVLink (the all-gather of the updated parameters, fused into
+// the optimizer kernel: no separate collective, no re-read).  Grid-stride over 16-byte
+// groups of the shard-local index space; a running bucket index maps j -> flat p index.
+struct Zero1Params {
+    const void* g;                  // staging half: shard-local reduced gradients
+    float* m; float* v;             // shard-local moments
+    float* p[kMaxRanks];            // every rank's flat p (index rank = own)
+    const BucketDev* buckets;
+    int nb, n, rank, barriers;
+    int64_t L;                      // shard elements
+    AdamScalars s;
+    Pads pads;
+    uint32_t epoch;
+    volatile float* hp_rec;
+    volatile int64_t* hp_tag;
+    int64_t step;
+};
+
+template <typename G, int N>
+__global__ void __launch_bounds__(256) adamw_zero1_kernel(const Zero1Params P) {
+    int b = 0;
+    const int64_t groups = P.L / 4;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < groups;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = q * 4;
+        while (b + 1 < P.nb && j >= P.buckets[b + 1].shard_off) ++b;
+        const BucketDev B = P.buckets[b];
+        const int64_t flat = B.off + (int64_t)P.rank * (B.padded / P.n) + (j - B.shard_off);
+        float4 g;
+        if constexpr (std::is_same<G, F32Tag>::value) {
+            g = __ldcs(reinterpret_cast<const float4*>((const float*)P.g + j));
+        } else {
+            const uint2 w = __ldcs(reinterpret_cast<const uint2*>((const uint16_t*)P.g + j));
+            g = make_float4(bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y));
+        }
+        float4 p = __ldcs(reinterpret_cast<const float4*>(P.p[P.rank] + flat));
+        float4 m = __ldcs(reinterpret_cast<const float4*>(P.m + j));
+        float4 v = __ldcs(reinterpret_cast<const float4*>(P.v + j));
+        adamw_elem(g.x, P.s, p.x, m.x, v.x);
+        adamw_elem(g.y, P.s, p.y, m.y, v.y);
+        adamw_elem(g.z, P.s, p.z, m.z, v.z);
+        adamw_elem(g.w, P.s, p.w, m.w, v.w);
+        __stcs(reinterpret_cast<float4*>(P.m + j), m);
+        __stcs(reinterpret_cast<float4*>(P.v + j), v);
+        const uint4 pw = make_uint4(__float_as_uint(p.x), __float_as_uint(p.y), __float_as_uint(p.z),
+                                    __float_as_uint(p.w));
+#pragma unroll
+        for (int k = 0; k < N; ++k) st_v4(P.p[k] + flat, pw);   // own p + all-gather
+    }
+    if (P.hp_rec && blockIdx.x == 0 && threadIdx.x == 0) {
+        const float* sf = &P.s.c1;
+        for (int k = 0; k < 10; ++k) P.hp_rec[k] = sf[k];
+        __threadfence_system();
+        *P.hp_tag = P.step;
+    }
+    if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 1);   // every shard landed everywhere
+}
+
 // ------------------------------------------------------------------ shard gather/scatter
 // Shard-local index j of rank r <-> flat index off_b + r*E_b/n + (j - shard_off_b).
 // dir 0 (snapshot): flat device p/m/v of this rank -> shard-local dst arrays.
@@ -608,6 +673,7 @@ struct ShardCopyParams {
     float* dst[3][kMaxRanks];   // dir 1: per-rank flat buffers; dir 0: [k][0] shard-local
     const BucketDev* buckets;
     int nb, n, rank, dir, barriers;
+    int mv_local;               // ZeRO-1: m, v are shard-local arrays of this rank only
     int64_t shard_nvec;         // shard-local 16-byte vectors of fp32
     Pads pads;
     uint32_t epoch;
@@ -624,8 +690,11 @@ __global__ void __launch_bounds__(256) shard_copy_kernel(const ShardCopyParams P
         const int64_t flat = B.off + (int64_t)P.rank * (B.padded / P.n) + (j - B.shard_off);
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
+            const bool local = P.mv_local && a > 0;   // shard-local m/v (ZeRO-1)
             if (P.dir == 0) {
-                st_v4(P.dst[a][0] + j, ld_v4(P.src[a] + flat));
+                st_v4(P.dst[a][0] + j, ld_v4(P.src[a] + (local ? j : flat)));
+            } else if (local) {
+                st_v4(P.dst[a][P.rank] + j, ld_v4(P.src[a] + j));
             } else {
                 const uint4 x = ld_v4(P.src[a] + j);
                 for (int k = 0; k < P.n; ++k) st_v4(P.dst[a][k] + flat, x);
@@ -641,16 +710,17 @@ __global__ void __launch_bounds__(256) compare_kernel(const float* __restrict__ 
                                                       const float* __restrict__ m, const float* __restrict__ v,
                                                       const BucketDev* __restrict__ buckets, int nb, int n,
                                                       int rank, int64_t shard_n,
-                                                      unsigned long long* first_bad) {
+                                                      unsigned long long* first_bad, int mv_local) {
     int b = 0;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < shard_n;
          j += (int64_t)gridDim.x * blockDim.x) {
         while (b + 1 < nb && j >= buckets[b + 1].shard_off) ++b;
         const BucketDev B = buckets[b];
         const int64_t flat = B.off + (int64_t)rank * (B.padded / n) + (j - B.shard_off);
+        const int64_t mi = mv_local ? j : flat;
         if (__float_as_uint(sp[j]) != __float_as_uint(p[flat]) ||
-            __float_as_uint(sm[j]) != __float_as_uint(m[flat]) ||
-            __float_as_uint(sv[j]) != __float_as_uint(v[flat]))
+            __float_as_uint(sm[j]) != __float_as_uint(m[mi]) ||
+            __float_as_uint(sv[j]) != __float_as_uint(v[mi]))
             atomicMin(first_bad, (unsigned long long)flat);
     }
 }

@@ -102,6 +102,8 @@ struct cm_ctx {
     std::string err;
     int n = 1, rank = 0, dev = 0, D = 2, dtype = 0, es = 4;
     bool no_tap = false, attach = false, ce_tap = false, no_shadow = false, staged_tap = false;
+    bool zero1 = false;                   // CM_FLAG_ZERO1: sharded optimizer state
+    int zero1_blocks = 296;
     void* stage_buf[2] = {};              // default tap: HBM staging of the reduced shard
     cudaEvent_t ev_stage_free[2] = {};    // staging half drained to the host ring
     cudaEvent_t ev_ar_done[2] = {};       // all all-reduce kernels of the half's iteration done
@@ -357,6 +359,24 @@ static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaSt
     return CM_OK;
 }
 
+template <typename G>
+static void launch_zero1_t(int n, int grid, cudaStream_t s, const Zero1Params& Z) {
+    switch (n) {
+        case 1: adamw_zero1_kernel<G, 1><<<grid, 256, 0, s>>>(Z); break;
+        case 2: adamw_zero1_kernel<G, 2><<<grid, 256, 0, s>>>(Z); break;
+        case 3: adamw_zero1_kernel<G, 3><<<grid, 256, 0, s>>>(Z); break;
+        case 4: adamw_zero1_kernel<G, 4><<<grid, 256, 0, s>>>(Z); break;
+        case 5: adamw_zero1_kernel<G, 5><<<grid, 256, 0, s>>>(Z); break;
+        case 6: adamw_zero1_kernel<G, 6><<<grid, 256, 0, s>>>(Z); break;
+        case 7: adamw_zero1_kernel<G, 7><<<grid, 256, 0, s>>>(Z); break;
+        default: adamw_zero1_kernel<G, 8><<<grid, 256, 0, s>>>(Z); break;
+    }
+}
+static void launch_zero1(cm_ctx* c, const Zero1Params& Z, int grid, cudaStream_t s) {
+    if (c->dtype == CM_F32) launch_zero1_t<F32Tag>(c->n, grid, s, Z);
+    else launch_zero1_t<BF16Tag>(c->n, grid, s, Z);
+}
+
 static cm_status publish(cm_ctx* c, volatile int64_t* host_field, int64_t value, cudaStream_t s) {
     // device alias of a header field
     volatile int64_t* d = (volatile int64_t*)(c->seg_dev + ((char*)host_field - c->seg));
@@ -507,6 +527,9 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
     c->ce_tap = (cfg->flags & CM_FLAG_TAP_COPYENGINE) != 0;
     // default tap = staged; CM_FLAG_TAP_DIRECT = kernel stores straight into the host ring
     c->staged_tap = (cfg->flags & CM_FLAG_TAP_DIRECT) == 0 && !c->ce_tap;
+    c->zero1 = (cfg->flags & CM_FLAG_ZERO1) != 0;
+    if (c->zero1 && (c->ce_tap || !c->staged_tap))
+        return fail(c, CM_ERR_CONFIG, "CM_FLAG_ZERO1 needs the staged tap (no TAP_DIRECT / TAP_COPYENGINE)");
     c->shadow_place = cfg->shadow_place;
     c->K = cfg->persist_every <= 1 ? 1 : cfg->persist_every;
     if (c->shadow_place == CM_SHADOW_DEVICE) c->K = 1;
@@ -584,6 +607,9 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
     c->shadow_blocks = c->sms * 2;
     c->misc_blocks = c->sms * 4;
     c->tma_blocks = c->sms;     // one 192 KB-smem block per SM
+    int zocc = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&zocc, adamw_zero1_kernel<F32Tag, 8>, 256, 0);
+    c->zero1_blocks = std::min(c->sms * std::max(zocc, 1), kMaxBarrierBlocks);
     int wocc = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wocc, adamw_wt_kernel<F32Tag>, kAdamThreads, 0);
     c->wt_blocks = c->sms * std::max(wocc, 1);
@@ -711,6 +737,7 @@ static cm_status snapshot_state(cm_ctx* c, int half, cudaStream_t s) {
     P.rank = c->rank;
     P.dir = 0;
     P.barriers = 0;
+    P.mv_local = c->zero1 ? 1 : 0;
     P.shard_nvec = c->shard_numel / 4;
     int64_t want = (P.shard_nvec + 255) / 256;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c->misc_blocks));
@@ -823,7 +850,7 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     }
     if (c->issued[bucket]) return fail(c, CM_ERR_STATE, "bucket %d of iteration %lld issued twice", bucket, (long long)t);
     const int slot = (int)(t % c->D);
-    if (c->no_tap && c->n == 1) {          // nothing to reduce, gather or tap
+    if (c->no_tap && c->n == 1 && !c->zero1) {   // nothing to reduce, gather or tap
         c->issued[bucket] = 1;
         c->issued_count++;
         return CM_OK;
@@ -851,12 +878,13 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     P.epoch = ++c->epoch;
     P.rank = c->rank;
     P.barriers = c->barriers ? 1 : 0;
-    P.ag = c->n > 1 ? 1 : 0;
+    P.ag = (c->n > 1 && !c->zero1) ? 1 : 0;   // ZeRO-1 gathers the updated params instead
     // tap modes: fused (kernel stores to the host ring), staged (kernel stores to an HBM
     // staging half, a copy engine drains it to the ring), copy-engine (CE reads the reduced
     // shard back from the grad buffer after the kernel)
     const bool fused_tap = !c->no_tap && !c->ce_tap && !c->staged_tap;
-    const bool staged = !c->no_tap && c->staged_tap;
+    // ZeRO-1 always reduces into the staging half: the sharded AdamW reads it from there
+    const bool staged = (!c->no_tap && c->staged_tap) || c->zero1;
     if (staged) {
         if (!c->stage_buf[0]) {
             for (int i = 0; i < 2; ++i) {
@@ -950,7 +978,31 @@ cm_status cm_apply_step(cm_ctx* c, int64_t step, const cm_adamw* hp, void* strea
         P.step = step;
     }
     cm_status st;
-    {
+    if (c->zero1) {
+        // ZeRO-1: AdamW on this rank's shard (reduced grads in staging half (step-1)&1),
+        // fused with the NVLink all-gather of the updated parameters
+        Zero1Params Z{};
+        Z.g = c->stage_buf[(step - 1) & 1];
+        Z.m = c->m; Z.v = c->v;
+        for (int k = 0; k < c->n; ++k) Z.p[k] = c->peer_p[k];
+        Z.buckets = c->d_buckets;
+        Z.nb = (int)c->buckets.size();
+        Z.n = c->n; Z.rank = c->rank; Z.barriers = c->barriers ? 1 : 0;
+        Z.L = c->shard_numel;
+        Z.s = a;
+        Z.pads = c->pads;
+        Z.epoch = ++c->epoch;
+        Z.hp_rec = P.hp_rec; Z.hp_tag = P.hp_tag; Z.step = step;
+        const int64_t want = (Z.L / 4 + 255) / 256;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c->zero1_blocks));
+        {
+            TimedScope ts(c, 1, S(stream));
+            launch_zero1(c, Z, grid, S(stream));
+        }
+        c->launches++;
+        cudaError_t e = cudaGetLastError();
+        st = e == cudaSuccess ? CM_OK : fail(c, CM_ERR_CUDA, "zero1 launch: %s", cudaGetErrorString(e));
+    } else {
         TimedScope ts(c, 1, S(stream));
         st = launch_adamw(c, P, c->adam_blocks, S(stream));
     }
@@ -1137,7 +1189,12 @@ cm_status cm_init_state(cm_ctx* c, uint64_t seed, void* stream) {
     }();
     const int64_t nvec = c->P_pad / 4;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, c->misc_blocks));
-    init_state_kernel<<<grid, 256, 0, S(stream)>>>(c->p, c->m, c->v, nvec, c->d_buckets, (int)c->buckets.size(), K);
+    init_state_kernel<<<grid, 256, 0, S(stream)>>>(c->p, c->zero1 ? nullptr : c->m, c->zero1 ? nullptr : c->v, nvec,
+                                                   c->d_buckets, (int)c->buckets.size(), K);
+    if (c->zero1) {
+        CU(cudaMemsetAsync(c->m, 0, (size_t)c->shard_numel * 4, S(stream)));
+        CU(cudaMemsetAsync(c->v, 0, (size_t)c->shard_numel * 4, S(stream)));
+    }
     c->launches++;
     CHECK_LAUNCH();
     return CM_OK;
@@ -1166,7 +1223,8 @@ cm_status cm_verify(cm_ctx* c, int64_t* mismatch, void* stream) {
         const float* src[3];
         for (int a = 0; a < 3; ++a) src[a] = which == 0 ? c->sd[h][a] : to_dev(c, c->sh[hhalf][a]);
         compare_kernel<<<grid, 256, 0, s>>>(src[0], src[1], src[2], c->p, c->m, c->v, c->d_buckets,
-                                            (int)c->buckets.size(), c->n, c->rank, c->shard_numel, c->d_bad);
+                                            (int)c->buckets.size(), c->n, c->rank, c->shard_numel, c->d_bad,
+                                            c->zero1 ? 1 : 0);
         c->launches++;
         CHECK_LAUNCH();
     }
@@ -1306,6 +1364,7 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     P.rank = c->rank;
     P.dir = 1;
     P.barriers = c->barriers ? 1 : 0;
+    P.mv_local = c->zero1 ? 1 : 0;
     P.shard_nvec = c->shard_numel / 4;
     P.pads = c->pads;
     P.epoch = ++c->epoch;

@@ -36,8 +36,10 @@ class Rank:
         # one allocation per flat buffer (CUDA IPC maps whole allocations)
         self.grad = torch.empty(self.padded, dtype=TORCH_DT[grad_dtype], device=dev)
         self.p = torch.empty(self.padded, dtype=torch.float32, device=dev)
-        self.m = torch.empty(self.padded, dtype=torch.float32, device=dev)
-        self.v = torch.empty(self.padded, dtype=torch.float32, device=dev)
+        # ZeRO-1 keeps only this rank's shard of the moments (shard-local order)
+        mv = self.padded // world_size if flags & cm.CM_FLAG_ZERO1 else self.padded
+        self.m = torch.empty(mv, dtype=torch.float32, device=dev)
+        self.v = torch.empty(mv, dtype=torch.float32, device=dev)
         self.ctx = cm.Context(world_size, rank, device, ring_depth, shadow_place, shm_name, flags, persist_every)
         self.blob = self.ctx.register_buckets(self.numel, grad_dtype, cap_bytes, self.grad.data_ptr(),
                                               self.p.data_ptr(), self.m.data_ptr(), self.v.data_ptr())

@@ -46,6 +46,8 @@ def run_arm(arm, args, rank, world, local):
             {"ce": cm.CM_FLAG_TAP_COPYENGINE, "direct": cm.CM_FLAG_TAP_DIRECT}.get(args.tap, 0))
         if arm == "ours_tap_only":                  # tap into the ring, no shadow replica
             flags |= cm.CM_FLAG_NO_SHADOW
+        if getattr(args, "zero1", False):
+            flags |= cm.CM_FLAG_ZERO1
         name = f"cmmm_{os.environ.get('MASTER_PORT', '0')}_{arm}"
         cd = CheckmateDDP(model, local, world, rank, shm_name=name, ring_depth=args.ring_depth,
                           persist_every=args.persist_every, flags=flags)

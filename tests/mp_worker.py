@@ -33,8 +33,20 @@ def t2np(t):
     return t.cpu().numpy()
 
 
-def check(R, ref, what):
+def shard_of(flat, plan, rank):
+    n = plan.world_size
+    return np.concatenate([flat[o + rank * (p // n): o + (rank + 1) * (p // n)]
+                           for o, p in zip(plan.bucket_off, plan.bucket_padded)])
+
+
+def check(R, ref, what, plan=None):
     r = R.r
+    if plan is not None:   # ZeRO-1: full p everywhere, shard-local m/v, no gradient all-gather
+        np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p), err_msg=f"{what}: p rank {R.rank_id}")
+        np.testing.assert_array_equal(bits(t2np(r.m)), bits(shard_of(ref.m, plan, R.rank_id)))
+        np.testing.assert_array_equal(bits(t2np(r.v)), bits(shard_of(ref.v, plan, R.rank_id)))
+        assert r.ctx.verify(R.stream) == -1, f"{what}: shadow != train on rank {R.rank_id}"
+        return
     np.testing.assert_array_equal(bits(t2np(r.grad)), bits(ref.R), err_msg=f"{what}: R rank {R.rank_id}")
     for nm, a, b in (("p", r.p, ref.p), ("m", r.m, ref.m), ("v", r.v, ref.v)):
         np.testing.assert_array_equal(bits(t2np(a)), bits(b), err_msg=f"{what}: {nm} rank {R.rank_id}")
@@ -53,13 +65,15 @@ def main():
     plan = O.Plan(numel, cap, 4 if dtype == cm.CM_F32 else 2, n)
     ref = O.Run(plan, seed=0, dtype=dtype, gscale=W.GRAD_SCALE, hp=HP_O)
     flags = cm.CM_FLAG_ATTACH if mode == "hardkill_phase2" else 0
+    if mode == "parity_zero1":
+        flags |= cm.CM_FLAG_ZERO1
     R = harness.DistRank(numel, dtype, cap, name, 2, cm.CM_SHADOW_HOST, flags)
     if mode.startswith("parity"):
         for t in range(6):
             R.step()
             ref.step()
             R.sync()
-            check(R, ref, f"iteration {t}")
+            check(R, ref, f"iteration {t}", plan if mode == "parity_zero1" else None)
     elif mode == "restore_soft":
         for _ in range(4):
             R.step()

@@ -489,3 +489,66 @@ def test_lagging_shadow_falls_back_from_staging_to_ring():
         np.testing.assert_array_equal(bits(sv), bits(ref.sv))
     finally:
         close(g)
+
+
+def _zero1_shard_of(flat, plan, rank):
+    """The oracle's flat array restricted to `rank`'s shard, in shard-local order."""
+    n = plan.world_size
+    out = []
+    for off, padded in zip(plan.bucket_off, plan.bucket_padded):
+        e = padded // n
+        out.append(flat[off + rank * e: off + (rank + 1) * e])
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_zero1_bit_exact(n, dtype):
+    """ZeRO-1 (f3): reduce-scatter + tap, AdamW on the own shard, fused parameter
+    all-gather.  Every rank's full p, its shard-local m/v and the shadow equal the oracle
+    (the unsharded definition) bit for bit."""
+    numel = TABLES["mixed"]
+    g = make_group(numel, n, dtype, flags=cm.CM_FLAG_ZERO1)
+    plan, ref = oracle_for(numel, n, dtype, 1 << 20)
+    try:
+        assert g.ranks[0].m.numel() == plan.total // n
+        for t in range(4):
+            g.step()
+            ref.step()
+            g.sync()
+            for r in g.ranks:
+                np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p), err_msg=f"p rank {r.rank} t {t}")
+                np.testing.assert_array_equal(bits(t2np(r.m)), bits(_zero1_shard_of(ref.m, plan, r.rank)))
+                np.testing.assert_array_equal(bits(t2np(r.v)), bits(_zero1_shard_of(ref.v, plan, r.rank)))
+                assert r.ctx.verify(g.stream) == -1
+            np.testing.assert_array_equal(bits(ring_flat(g, t % 2)), bits(ref.T), err_msg=f"tap t {t}")
+    finally:
+        close(g)
+
+
+def test_zero1_restore_bit_exact():
+    numel = TABLES["ragged"]
+    n = 4
+    g = make_group(numel, n, flags=cm.CM_FLAG_ZERO1, D=4)
+    plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
+    try:
+        for _ in range(5):
+            g.step()
+        g.sync()
+        for r in g.ranks:
+            r.p.fill_(float("nan")); r.m.fill_(float("nan")); r.v.fill_(float("nan"))
+        torch.cuda.synchronize()
+        assert [r.ctx.restore(g.stream) for r in g.ranks] == [5] * n
+        for _ in range(5):
+            ref.step()
+        g.t = 5
+        for _ in range(3):
+            g.step()
+            ref.step()
+        g.sync()
+        for r in g.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            np.testing.assert_array_equal(bits(t2np(r.v)), bits(_zero1_shard_of(ref.v, plan, r.rank)))
+            assert r.ctx.verify(g.stream) == -1
+    finally:
+        close(g)
