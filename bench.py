@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--zero1", action="store_true",
                     help="sharded AdamW state: reduce-scatter + tap, AdamW on the own shard fused with the "
                          "NVLink all-gather of the updated parameters (SURVEY 8 f3)")
+    ap.add_argument("--no-variants", action="store_true", help="skip the ZeRO-1 variant timing (N>1)")
     ap.add_argument("--no-model", action="store_true",
                     help="skip the GPT-2 model-mode arms (real fwd/bwd; checkpoint overhead vs NCCL DDP)")
     ap.add_argument("--model-steps", type=int, default=10)
@@ -259,7 +260,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     kern = {}
     ar_ms = kms[0] / max(kcnt[0], 1)
     Sb = S_bytes / nb                                            # average bucket bytes
-    ar_nvl = (n - 1) / n * Sb                                    # per direction, per GPU
+    ar_nvl = 2 * (n - 1) / n * Sb * (0.5 if args.zero1 else 1.0)  # per direction per GPU = busBW bytes (RS only in ZeRO-1)
     ar_hbm = 2 * Sb + (Sb / n if args.tap == "staged" else 0)    # local + peers' reads/writes (+ staging)
     if n == 1:
         ar_hbm = (2 * Sb) if args.tap == "staged" else Sb        # copy to staging / read for a direct tap
@@ -276,11 +277,26 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     ent["frac"] = ent["achieved"] / ent["peak"]
     kern["rs_tap_ag"] = ent
     ad_ms = kms[1] / max(kcnt[1], 1)
-    ad_bytes = P * (es + 24)
-    kern["adamw_step"] = {"avg_ms": ad_ms, "launches": kcnt[1], "share": kms[1] / ms, "bound": "hbm",
-                          "achieved": ad_bytes / (ad_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                          "bytes_per_launch": ad_bytes, "peak_source": hbm_src}
-    kern["adamw_step"]["frac"] = kern["adamw_step"]["achieved"] / hbm_peak
+    if args.zero1:
+        # sharded AdamW on L = P/n elements, fused with the parameter all-gather: HBM es+24
+        # per shard element; NVLink 4 (n-1) B per shard element out (the p stores to peers)
+        ad_bytes = L * (es + 24)
+        ad_nvl = L * 4 * (n - 1)
+        kern["adamw_step"] = {"avg_ms": ad_ms, "launches": kcnt[1], "share": kms[1] / ms,
+                              "hbm_GBps": ad_bytes / (ad_ms * 1e-3) / 1e9,
+                              "nvlink_out_GBps": ad_nvl / (ad_ms * 1e-3) / 1e9,
+                              "bound": "nvlink" if n > 1 else "hbm",
+                              "achieved": (ad_nvl if n > 1 else ad_bytes) / (ad_ms * 1e-3) / 1e9,
+                              "peak": NVLINK_PEAK_GBS if n > 1 else hbm_peak, "unit": "GB/s",
+                              "bytes_per_launch": ad_nvl if n > 1 else ad_bytes,
+                              "what": "ZeRO-1: AdamW on the own shard + fused NVLink parameter all-gather"}
+        kern["adamw_step"]["frac"] = kern["adamw_step"]["achieved"] / kern["adamw_step"]["peak"]
+    else:
+        ad_bytes = P * (es + 24)
+        kern["adamw_step"] = {"avg_ms": ad_ms, "launches": kcnt[1], "share": kms[1] / ms, "bound": "hbm",
+                              "achieved": ad_bytes / (ad_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                              "bytes_per_launch": ad_bytes, "peak_source": hbm_src}
+        kern["adamw_step"]["frac"] = kern["adamw_step"]["achieved"] / hbm_peak
     sh_ms = kms[2] / max(kcnt[2], 1)
     sh_hbm = L * (es + 24)
     sh_d2h = L * 12 / K if place == cm.CM_SHADOW_HOST else 0.0
@@ -486,6 +502,16 @@ def main():
     res = run_ours(args, rank, world, local, name, numel, dtype, cap)
     base = None if args.no_baseline else run_nccl_baseline(args, rank, world, local, numel, dtype, cap)
     ours_nockpt = None if args.no_baseline else run_ours_nockpt(args, rank, world, local, numel, dtype, cap)
+    variants = {}
+    if not args.zero1 and not args.no_variants and world > 1:
+        # the ZeRO-1 variant of the same checkpointed step: sharded AdamW fused
+        # with the NVLink parameter all-gather; same per-element arithmetic
+        import copy
+        zargs = copy.copy(args)
+        zargs.zero1, zargs.no_e2e = True, True
+        zres = run_ours(zargs, rank, world, local, name, numel, dtype, cap)
+        variants["zero1"] = {"ms_per_step": zres["ms_step"], "value": zres["iters_per_s"] * world,
+                             "shadow_bit_identical": zres["shadow_bit_identical"]}
     model = None
     if not args.no_model and args.workload == "gpt2":
         import types
@@ -516,7 +542,7 @@ def main():
                        "iters_per_s": res["iters_per_s"]},
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res.get("e2e"),
             "gpu_launches": res["launches"], "clocks": res["clocks"],
-            "nockpt_nccl": base, "nockpt_ours": ours_nockpt, "model_mode": model,
+            "nockpt_nccl": base, "nockpt_ours": ours_nockpt, "model_mode": model, "variants": variants,
             "ckpt_overhead_pct_vs_nccl": overhead,
             "shadow_bit_identical": res["shadow_bit_identical"], "kernels": res["kernels"],
             "host_link_GBps": res["host_link_GBps"],
