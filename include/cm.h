@@ -172,6 +172,23 @@ cm_status cm_connect(cm_ctx *ctx, const void *peer_blobs, size_t blob_len);
  * shadow segment is NOT unlinked (it is the restore source); see cm_unlink_shadow.     */
 cm_status cm_finalize(cm_ctx *ctx);
 cm_status cm_unlink_shadow(const char *shm_name, int32_t rank);
+
+/* Shadow persistence (SPEC.md:371-374 CheckpointFile, SPEC.md:446
+ * CRC-32).  Host-only, no device or context needed.
+ * cm_shadow_save -- write rank `rank`'s shadow segment (snapshot halves, tapped-gradient
+ *   ring, step records, tap flags: everything restore needs) to `path` as a
+ *   CheckpointFile: a 64-byte header (magic, version, CRC-32 of the payload, payload
+ *   bytes, layout hash, world size, rank, shadow step) + the segment bytes.  Written to
+ *   `path`.tmp, fsync'd, renamed.  Call it while the segment is quiescent (after cm_join
+ *   and a stream sync, or after the trainer died).  CM_ERR_ARG if the segment is missing.
+ * cm_shadow_load -- verify a CheckpointFile (magic, rank, size, CRC-32, layout hash) and
+ *   recreate the shm segment from it; a context created with CM_FLAG_ATTACH then restores
+ *   from it (e.g. on a new host).  CM_ERR_INVARIANT if the CRC or layout does not match
+ *   (the segment is not created), CM_ERR_ARG for an unreadable / malformed file.
+ * cm_crc32 -- the checksum used (IEEE 802.3 / zlib CRC-32), exposed for tests.          */
+cm_status cm_shadow_save(const char *shm_name, int32_t rank, const char *path);
+cm_status cm_shadow_load(const char *path, const char *shm_name, int32_t rank);
+uint32_t cm_crc32(const void *data, size_t n);
 const char *cm_last_error(const cm_ctx *ctx);
 
 /* ------------------------------------------------------------------ hot path

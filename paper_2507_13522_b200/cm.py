@@ -27,7 +27,8 @@ CM_FLAG_TAP_DIRECT = 1 << 4     # default tap is "staged" (HBM staging + copy-en
 EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
            "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step",
            "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_get_info",
-           "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_set_param", "cm_join"]
+           "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_set_param", "cm_join", "cm_shadow_save", "cm_shadow_load",
+           "cm_crc32"]
 
 
 class cm_config(C.Structure):
@@ -94,10 +95,14 @@ def lib():
         L.cm_ring_view.argtypes = [P, C.c_int32, C.POINTER(P)]
         L.cm_set_param.argtypes = [P, C.c_char_p, C.c_int64]
         L.cm_join.argtypes = [P, P]
+        L.cm_shadow_save.argtypes = [C.c_char_p, C.c_int32, C.c_char_p]
+        L.cm_shadow_load.argtypes = [C.c_char_p, C.c_char_p, C.c_int32]
+        L.cm_crc32.argtypes = [C.c_void_p, C.c_size_t]
         L.cm_timing.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         for name in EXPORTS:
-            if name not in ("cm_blob_size", "cm_last_error"):
+            if name not in ("cm_blob_size", "cm_last_error", "cm_crc32"):
                 getattr(L, name).restype = C.c_int     # cm_status
+        L.cm_crc32.restype = C.c_uint32
         _lib = L
     return _lib
 
@@ -122,6 +127,24 @@ def plan_buckets(numel, grad_dtype, cap_bytes, world_size):
 
 def unlink_shadow(name, rank):
     return lib().cm_unlink_shadow(name.encode(), int(rank))
+
+
+def shadow_save(name, rank, path):
+    """Persist a rank's shadow segment to a CheckpointFile (CRC-32)."""
+    st = lib().cm_shadow_save(name.encode(), int(rank), str(path).encode())
+    if st != CM_OK:
+        raise CMError(st, f"cm_shadow_save({name}, {rank}, {path})")
+
+
+def shadow_load(path, name, rank):
+    """Recreate a rank's shadow segment from a CheckpointFile (CRC-32 verified)."""
+    st = lib().cm_shadow_load(str(path).encode(), name.encode(), int(rank))
+    if st != CM_OK:
+        raise CMError(st, f"cm_shadow_load({path}, {name}, {rank})")
+
+
+def crc32(data: bytes) -> int:
+    return int(lib().cm_crc32(data, len(data)))
 
 
 def _stream_ptr(stream):

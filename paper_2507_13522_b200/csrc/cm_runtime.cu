@@ -1429,6 +1429,133 @@ cm_status cm_ring_view(const cm_ctx* c, int32_t slot, void** grads) {
     return CM_OK;
 }
 
+// ---------------------------------------------------------------- CheckpointFile (f4)
+// SPEC.md:371-374 (CheckpointFile, CRC-32 checksum): the host shadow of one
+// rank -- snapshot halves, the tapped-gradient ring, step records and flags -- persisted
+// to a file and recreated from it (restore then works on another host, or after the
+// host's shared memory is gone).  CRC-32 = IEEE 802.3 (reflected 0xEDB88320), the zlib
+// checksum, computed slice-by-8.
+namespace {
+struct FileHeader {
+    uint64_t magic;        // kFileMagic
+    uint32_t version, crc32;
+    uint64_t payload_bytes, layout_hash;
+    int32_t world_size, rank;
+    int64_t shadow_step;
+    uint64_t reserved[2];
+};
+static_assert(sizeof(FileHeader) == 64, "file header");
+constexpr uint64_t kFileMagic = 0x454C49465442434Bull;   // bytes "KCBTFILE"
+
+uint32_t crc_tab[8][256];
+void crc_init() {
+    static bool done = false;
+    if (done) return;
+    for (uint32_t i = 0; i < 256; ++i) {
+        uint32_t c = i;
+        for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+        crc_tab[0][i] = c;
+    }
+    for (uint32_t i = 0; i < 256; ++i)
+        for (int t = 1; t < 8; ++t) crc_tab[t][i] = (crc_tab[t - 1][i] >> 8) ^ crc_tab[0][crc_tab[t - 1][i] & 0xFF];
+    done = true;
+}
+uint32_t crc32_update(uint32_t crc, const unsigned char* p, size_t n) {
+    crc = ~crc;
+    while (n >= 8) {
+        uint32_t a, b;
+        memcpy(&a, p, 4);
+        memcpy(&b, p + 4, 4);
+        a ^= crc;
+        crc = crc_tab[7][a & 0xFF] ^ crc_tab[6][(a >> 8) & 0xFF] ^ crc_tab[5][(a >> 16) & 0xFF] ^
+              crc_tab[4][a >> 24] ^ crc_tab[3][b & 0xFF] ^ crc_tab[2][(b >> 8) & 0xFF] ^
+              crc_tab[1][(b >> 16) & 0xFF] ^ crc_tab[0][b >> 24];
+        p += 8;
+        n -= 8;
+    }
+    while (n--) crc = crc_tab[0][(crc ^ *p++) & 0xFF] ^ (crc >> 8);
+    return ~crc;
+}
+}  // namespace
+
+uint32_t cm_crc32(const void* data, size_t n) {
+    crc_init();
+    return crc32_update(0, (const unsigned char*)data, n);
+}
+
+cm_status cm_shadow_save(const char* shm_name, int32_t rank, const char* path) {
+    if (!shm_name || !path) return CM_ERR_ARG;
+    crc_init();
+    char name[256];
+    snprintf(name, sizeof name, "/%s.r%d", shm_name, rank);
+    int fd = shm_open(name, O_RDONLY, 0);
+    if (fd < 0) return CM_ERR_ARG;
+    struct stat st;
+    if (fstat(fd, &st) != 0 || (size_t)st.st_size < sizeof(SegHeader)) { close(fd); return CM_ERR_ARG; }
+    const size_t size = (size_t)st.st_size;
+    void* mp = mmap(nullptr, size, PROT_READ, MAP_SHARED, fd, 0);
+    close(fd);
+    if (mp == MAP_FAILED) return CM_ERR_ARG;
+    const SegHeader* h = (const SegHeader*)mp;
+    cm_status rc = CM_OK;
+    FILE* f = nullptr;
+    if (h->magic != kMagic || h->total != size) { rc = CM_ERR_ARG; goto done; }
+    {
+        FileHeader fh{};
+        fh.magic = kFileMagic;
+        fh.version = 1;
+        fh.payload_bytes = size;
+        fh.layout_hash = h->layout_hash;
+        fh.world_size = h->world_size;
+        fh.rank = h->rank;
+        fh.shadow_step = h->shadow_step;
+        fh.crc32 = crc32_update(0, (const unsigned char*)mp, size);
+        std::string tmp = std::string(path) + ".tmp";
+        f = fopen(tmp.c_str(), "wb");
+        if (!f) { rc = CM_ERR_ARG; goto done; }
+        bool ok = fwrite(&fh, sizeof fh, 1, f) == 1 && fwrite(mp, 1, size, f) == size;
+        ok = (fflush(f) == 0) && ok && (fsync(fileno(f)) == 0);
+        ok = (fclose(f) == 0) && ok;
+        f = nullptr;
+        if (!ok || rename(tmp.c_str(), path) != 0) { unlink(tmp.c_str()); rc = CM_ERR_ARG; }
+    }
+done:
+    munmap(mp, size);
+    return rc;
+}
+
+cm_status cm_shadow_load(const char* path, const char* shm_name, int32_t rank) {
+    if (!shm_name || !path) return CM_ERR_ARG;
+    crc_init();
+    FILE* f = fopen(path, "rb");
+    if (!f) return CM_ERR_ARG;
+    FileHeader fh{};
+    if (fread(&fh, sizeof fh, 1, f) != 1 || fh.magic != kFileMagic || fh.version != 1 || fh.rank != rank ||
+        fh.payload_bytes < sizeof(SegHeader)) {
+        fclose(f);
+        return CM_ERR_ARG;
+    }
+    char name[256];
+    snprintf(name, sizeof name, "/%s.r%d", shm_name, rank);
+    shm_unlink(name);
+    int fd = shm_open(name, O_RDWR | O_CREAT | O_EXCL, 0600);
+    if (fd < 0) { fclose(f); return CM_ERR_ARG; }
+    cm_status rc = CM_OK;
+    void* mp = MAP_FAILED;
+    if (ftruncate(fd, (off_t)fh.payload_bytes) != 0) rc = CM_ERR_ARG;
+    if (rc == CM_OK) mp = mmap(nullptr, fh.payload_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (mp == MAP_FAILED) rc = CM_ERR_ARG;
+    if (rc == CM_OK && fread(mp, 1, fh.payload_bytes, f) != fh.payload_bytes) rc = CM_ERR_ARG;
+    if (rc == CM_OK && crc32_update(0, (const unsigned char*)mp, fh.payload_bytes) != fh.crc32)
+        rc = CM_ERR_INVARIANT;   // corrupted checkpoint: refuse it
+    if (rc == CM_OK && ((const SegHeader*)mp)->layout_hash != fh.layout_hash) rc = CM_ERR_INVARIANT;
+    if (mp != MAP_FAILED) munmap(mp, fh.payload_bytes);
+    fclose(f);
+    if (rc != CM_OK) shm_unlink(name);
+    return rc;
+}
+
 cm_status cm_unlink_shadow(const char* name, int32_t rank) {
     if (!name) return CM_ERR_ARG;
     char buf[256];

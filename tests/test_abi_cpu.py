@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "cm.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(cm_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(cm_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_the_six_paper_calls():

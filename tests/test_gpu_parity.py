@@ -552,3 +552,47 @@ def test_zero1_restore_bit_exact():
             assert r.ctx.verify(g.stream) == -1
     finally:
         close(g)
+
+
+def test_checkpoint_file_save_load_restore(tmp_path):
+    """f4: persist every rank's host shadow to a CheckpointFile (CRC-32), drop the shared
+    memory, recreate it from the files (as on a new host), attach, restore, continue:
+    bit-exact vs the oracle."""
+    numel = TABLES["ragged"]
+    n = 2
+    g = make_group(numel, n, D=4)
+    g.ranks[0].ctx  # noqa: B018
+    plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
+    try:
+        for _ in range(5):
+            g.step()
+        g.sync()
+        for r in g.ranks:
+            r.ctx.join(g.stream)
+        g.stream.synchronize()
+        for r in range(n):
+            cm.shadow_save(g._shm, r, tmp_path / f"rank{r}.ckpt")
+    finally:
+        close(g)                                   # segments unlinked: only the files remain
+    name = _name()
+    for r in range(n):
+        cm.shadow_load(tmp_path / f"rank{r}.ckpt", name, r)
+    g2 = harness.VirtualGroup(numel, n, 0, cm.CM_F32, 1 << 20, name, 4, cm.CM_SHADOW_HOST, cm.CM_FLAG_ATTACH, 0)
+    g2._shm = name
+    try:
+        for r in g2.ranks:
+            r.p.fill_(float("nan"))
+        torch.cuda.synchronize()
+        assert [r.ctx.restore(g2.stream) for r in g2.ranks] == [5] * n
+        for _ in range(5):
+            ref.step()
+        g2.t = 5
+        for _ in range(3):
+            g2.step()
+            ref.step()
+        g2.sync()
+        for r in g2.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            assert r.ctx.verify(g2.stream) == -1
+    finally:
+        close(g2)
