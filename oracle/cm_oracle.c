@@ -350,6 +350,83 @@ void cmo_run_sample(uint64_t seed, int32_t n, int32_t dtype, int32_t gscale,
 }
 
 /* ------------------------------------------------------------------------- */
+/* 7b. SGD with momentum.  PAPER.md:307 (sec 4.2.4) names SGD*/
+/* among the functional optimizers the shadow can replay     */
+/* ([OP] sgd_step) fixes the update: velocity' = momentum*velocity + g,        */
+/* p' = p - lr*velocity' (momentum = 0 gives p' = p - lr*g).                   */
+/* Reading R27: g = R * inv_n first (R1, as for AdamW); when       */
+/* weight_decay != 0 the coupled L2 term of the classic SGD form is added to   */
+/* the gradient, d = g + wd*p (old p), a host-side choice recorded as wd_on;   */
+/* with wd = 0 the SPEC form is used unchanged.  The velocity is stored in the */
+/* m array (v is unused).  Scalars: fp64 -> fp32 once (R5).                    */
+/* out[0..4] = { mu, inv_n, lr, wd, wd_on (1.0f or 0.0f) }                      */
+/* ------------------------------------------------------------------------- */
+int cmo_sgd_scalars(double lr, double momentum, double wd, int32_t n, float *out) {
+    if (n < 1) return -1;
+    out[0] = (float)momentum;
+    out[1] = (float)(1.0 / (double)n);
+    out[2] = (float)lr;
+    out[3] = (float)wd;
+    out[4] = wd != 0.0 ? 1.0f : 0.0f;
+    return 0;
+}
+
+/*   g   = R * inv_n                                                           */
+/*   d   = g            (wd_on = 0)   |   d = g + wd*p   (wd_on = 1)            */
+/*   buf = mu*buf + d                                                          */
+/*   p   = p - lr*buf                                                          */
+static void sgd_elem(float R, const float *sc, float *p, float *buf) {
+    float mu = sc[0], inv_n = sc[1], lr = sc[2], wd = sc[3];
+    float g = R * inv_n;
+    float d = g;
+    if (sc[4] != 0.0f) d = g + wd * (*p);
+    float b = mu * (*buf) + d;
+    float pp = (*p) - lr * b;
+    *buf = b; *p = pp;
+}
+
+void cmo_sgd_f32(int64_t len, const float *R, const float *sc, float *p, float *buf) {
+    for (int64_t i = 0; i < len; ++i) sgd_elem(R[i], sc, &p[i], &buf[i]);
+}
+
+void cmo_sgd_bf16(int64_t len, const uint16_t *R, const float *sc, float *p, float *buf) {
+    for (int64_t i = 0; i < len; ++i) sgd_elem(bf16_to_f32(R[i]), sc, &p[i], &buf[i]);
+}
+
+/* Sampled SGD trajectory (same element independence as cmo_run_sample,       */
+/* PAPER.md:306-308).  Outputs p and the velocity buf after `steps` steps.     */
+void cmo_run_sample_sgd(uint64_t seed, int32_t n, int32_t dtype, int32_t gscale,
+                        int64_t t0, int64_t steps, double lr, double momentum, double wd,
+                        int64_t n_idx, const int64_t *idx, const uint8_t *used,
+                        float *p, float *buf, float *R_last) {
+    float sc[5];
+    cmo_sgd_scalars(lr, momentum, wd, n, sc);
+    for (int64_t k = 0; k < n_idx; ++k) {
+        p[k] = used[k] ? cmo_gen_p0(seed, (uint64_t)idx[k]) : 0.0f;
+        buf[k] = 0.0f; R_last[k] = 0.0f;
+    }
+    for (int64_t t = t0; t < t0 + steps; ++t) {
+        for (int64_t k = 0; k < n_idx; ++k) {
+            uint64_t i = (uint64_t)idx[k];
+            float R;
+            if (dtype == CMO_F32) {
+                float acc = used[k] ? cmo_gen_f32(seed, 0, (uint64_t)t, i, gscale) : 0.0f;
+                for (int32_t r = 1; r < n; ++r)
+                    acc = acc + (used[k] ? cmo_gen_f32(seed, (uint64_t)r, (uint64_t)t, i, gscale) : 0.0f);
+                R = acc;
+            } else {
+                float acc = used[k] ? cmo_gen_bf16val(seed, 0, (uint64_t)t, i, gscale) : 0.0f;
+                for (int32_t r = 1; r < n; ++r)
+                    acc = acc + (used[k] ? cmo_gen_bf16val(seed, (uint64_t)r, (uint64_t)t, i, gscale) : 0.0f);
+                R = bf16_to_f32(cmo_f32_to_bf16_rne(acc));
+            }
+            sgd_elem(R, sc, &p[k], &buf[k]);
+            R_last[k] = R;
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
 /* 8. Consolidation target for restore.  PAPER.md:313-314 ("uses a           */
 /* configurable timeout to consolidate shards into a complete checkpoint");   */
 /* R21 / SPEC.md:413-421: I = min over shards of the last completed step.     */

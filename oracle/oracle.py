@@ -79,6 +79,16 @@ def lib():
         L.cmo_run_sample.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
                                      C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                      C.c_int64, i64p, u8p, f32p, f32p, f32p, f32p]
+        L.cmo_sgd_scalars.restype = C.c_int
+        L.cmo_sgd_scalars.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int32, f32p]
+        L.cmo_sgd_f32.restype = None
+        L.cmo_sgd_f32.argtypes = [C.c_int64, f32p, f32p, f32p, f32p]
+        L.cmo_sgd_bf16.restype = None
+        L.cmo_sgd_bf16.argtypes = [C.c_int64, C.c_void_p, f32p, f32p, f32p]
+        L.cmo_run_sample_sgd.restype = None
+        L.cmo_run_sample_sgd.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
+                                         C.c_double, C.c_double, C.c_double, C.c_int64, i64p, u8p, f32p, f32p,
+                                         f32p]
         L.cmo_consolidate.restype = C.c_int64
         L.cmo_consolidate.argtypes = [C.c_int32, i64p]
         _lib = L
@@ -127,6 +137,22 @@ def scalars(step, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, wd=0.01, n=1) -> np.ndarr
     return out
 
 
+def sgd_scalars(lr=1e-2, momentum=0.9, wd=0.0, n=1) -> np.ndarray:
+    out = np.zeros(5, np.float32)
+    if lib().cmo_sgd_scalars(lr, momentum, wd, int(n), out) != 0:
+        raise ValueError("bad n")
+    return out
+
+
+def sgd(R, sc, p, buf, dtype=F32):
+    """SGD with momentum (reading R27), in place on float32 p, buf."""
+    if dtype == F32:
+        lib().cmo_sgd_f32(len(p), np.ascontiguousarray(R, np.float32), sc, p, buf)
+    else:
+        R = np.ascontiguousarray(R, np.uint16)
+        lib().cmo_sgd_bf16(len(p), R.ctypes.data, sc, p, buf)
+
+
 def gen_grads(plan: Plan, seed, rank, t, dtype, s=10) -> np.ndarray:
     out = np.zeros(plan.total, np.float32 if dtype == F32 else np.uint16)
     lib().cmo_fill_grads(seed, rank, t, dtype, s, plan.n_buckets, plan.bucket_off, plan.bucket_padded,
@@ -173,11 +199,17 @@ def adamw(R, sc, p, m, v, dtype=F32):
 
 class Run:
     """Whole-buffer oracle run of the path: per-rank grads -> R (rank-order sum) ->
-    tap T -> trainer AdamW and an independent shadow AdamW."""
+    tap T -> trainer AdamW and an independent shadow AdamW.
+    opt="sgd": the same path with SGD-momentum (hp keys lr, momentum, wd; the velocity
+    lives in m, v stays zero)."""
 
-    def __init__(self, plan: Plan, seed=0, dtype=F32, gscale=10, hp=None, shadow=True):
+    def __init__(self, plan: Plan, seed=0, dtype=F32, gscale=10, hp=None, shadow=True, opt="adamw"):
         self.plan, self.seed, self.dtype, self.gscale = plan, seed, dtype, gscale
-        self.hp = dict(lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, wd=0.01)
+        self.opt = opt
+        if opt == "sgd":
+            self.hp = dict(lr=1e-2, momentum=0.9, wd=0.0)
+        else:
+            self.hp = dict(lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, wd=0.01)
         if hp:
             self.hp.update(hp)
         n = plan.total
@@ -197,6 +229,15 @@ class Run:
         n = self.plan.world_size
         if grads is None:
             grads = [gen_grads(self.plan, self.seed, r, self.t, self.dtype, self.gscale) for r in range(n)]
+        if self.opt == "sgd":
+            self.R[:] = reduce_f32(grads) if self.dtype == F32 else reduce_bf16(grads)
+            self.T[:] = self.R                                   # tap: exactly R, once
+            sc = sgd_scalars(n=n, **self.hp)
+            sgd(self.R, sc, self.p, self.m, self.dtype)
+            if self.shadow:
+                sgd(self.T, sc, self.sp, self.sm, self.dtype)
+            self.t += 1
+            return grads
         sc = scalars(self.t + 1, n=n, **self.hp)
         null = None
         lib().cmo_iteration(n, self.plan.total, self.dtype, _ptrs(grads), sc, self.R.ctypes.data,
@@ -216,6 +257,16 @@ def run_sample(seed, n, dtype, gscale, steps, idx, used, t0=0, lr=1e-3, b1=0.9, 
     p, m, v, R = (np.zeros(k, np.float32) for _ in range(4))
     lib().cmo_run_sample(seed, n, dtype, gscale, t0, steps, lr, b1, b2, eps, wd, k, idx, used, p, m, v, R)
     return p, m, v, R
+
+
+def run_sample_sgd(seed, n, dtype, gscale, steps, idx, used, t0=0, lr=1e-2, momentum=0.9, wd=0.0):
+    """SGD-momentum trajectory of sampled flat indices -> (p, buf, R_last)."""
+    idx = np.ascontiguousarray(idx, np.int64)
+    used = np.ascontiguousarray(used, np.uint8)
+    k = len(idx)
+    p, b, R = (np.zeros(k, np.float32) for _ in range(3))
+    lib().cmo_run_sample_sgd(seed, n, dtype, gscale, t0, steps, lr, momentum, wd, k, idx, used, p, b, R)
+    return p, b, R
 
 
 def consolidate(last_steps) -> int:

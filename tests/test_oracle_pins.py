@@ -398,3 +398,85 @@ def test_restore_continues_bit_exact_and_consolidation_rule():
     assert O.consolidate([10, 10]) == 10
     assert O.consolidate([10, 9]) == 9
     assert O.consolidate([7, 9, 8, 7]) == 7
+
+
+# ----------------------------------------------------------------------------- SGD-momentum (f4)
+def test_sgd_spec_examples():
+    for line in _gold_lines("sgd_spec_examples.txt"):
+        p0, g, lr, mu, p1 = line.split()
+        p = np.array([int(p0, 16)], np.uint32).view(np.float32).copy()
+        buf = np.zeros(1, np.float32)
+        O.sgd(np.array([int(g, 16)], np.uint32).view(np.float32), O.sgd_scalars(lr=float(lr), momentum=float(mu)),
+              p, buf)
+        assert f32bits(p[0]) == int(p1, 16)
+
+
+@pytest.mark.parametrize("n", [1, 2, 8])
+def test_sgd_geometric_momentum_closed_form(n):
+    # mu = 1/2, constant g = 2^k, lr = 2^-10, wd = 0, buf_0 = 0: buf_t = g (2 - 2^(1-t)) and
+    # p_t = p_0 - lr g (2t - 2 + 2^(1-t)); every intermediate has few significant bits, so
+    # both are exact in binary32.  R = n*g checks that inv_n is applied first.
+    for k in (-3, 0, 4):
+        g = 2.0 ** k
+        p = np.full(4, 1.0, np.float32)
+        buf = np.zeros(4, np.float32)
+        sc = O.sgd_scalars(lr=2.0 ** -10, momentum=0.5, wd=0.0, n=n)
+        for t in range(1, 13):
+            O.sgd(np.full(4, n * g, np.float32), sc, p, buf)
+            assert np.all(buf == np.float32(g * (2.0 - 2.0 ** (1 - t)))), (k, t)
+            assert np.all(p == np.float32(1.0 - 2.0 ** -10 * g * (2 * t - 2 + 2.0 ** (1 - t)))), (k, t)
+
+
+def test_sgd_pure_weight_decay_closed_form():
+    # g = 0, mu = 0, wd = 1/2, lr = 1/2: d = p/2, buf = d, p' = p - p/4 = (3/4) p,
+    # so p_t = (3/4)^t exactly while 3^t < 2^24 (t <= 15)
+    p = np.ones(3, np.float32)
+    buf = np.zeros(3, np.float32)
+    sc = O.sgd_scalars(lr=0.5, momentum=0.0, wd=0.5)
+    for t in range(1, 16):
+        O.sgd(np.zeros(3, np.float32), sc, p, buf)
+        assert np.all(p == np.float32(0.75 ** t)), t
+    # zero gradient without decay is a fixed point
+    q = np.random.default_rng(0).standard_normal(100).astype(np.float32)
+    q0, b = q.copy(), np.zeros(100, np.float32)
+    O.sgd(np.zeros(100, np.float32), O.sgd_scalars(lr=0.1, momentum=0.9), q, b)
+    np.testing.assert_array_equal(q, q0)
+
+
+def test_sgd_multistep_vs_torch_fp64():
+    """Sanity vs torch.optim.SGD (momentum, coupled weight decay) in float64: tolerance only."""
+    rng = np.random.default_rng(6)
+    N = 5000
+    p0 = (rng.standard_normal(N) * 0.05).astype(np.float32)
+    grads = [(rng.standard_normal(N) * np.exp2(rng.integers(-12, 0, N))).astype(np.float32) for _ in range(20)]
+    p, buf = p0.copy(), np.zeros(N, np.float32)
+    tp = torch.nn.Parameter(torch.from_numpy(p0.astype(np.float64)))
+    opt = torch.optim.SGD([tp], lr=1e-2, momentum=0.9, weight_decay=1e-4, foreach=False)
+    sc = O.sgd_scalars(lr=1e-2, momentum=0.9, wd=1e-4)
+    for g in grads:
+        O.sgd(g, sc, p, buf)
+        tp.grad = torch.from_numpy(g.astype(np.float64))
+        opt.step()
+    ref = tp.detach().numpy()
+    assert np.max(np.abs(p - ref)) < 1e-6, np.max(np.abs(p - ref))
+    eb = opt.state[tp]["momentum_buffer"].numpy()
+    np.testing.assert_allclose(buf, eb, rtol=1e-5, atol=1e-5 * np.abs(eb).max())
+    assert np.max(np.abs(p - p0)) > 1e-3
+
+
+@pytest.mark.parametrize("dtype", [O.F32, O.BF16])
+def test_sgd_run_sample_matches_whole_buffer_and_shadow(dtype):
+    es = 4 if dtype == O.F32 else 2
+    plan = O.Plan(W.numels(W.c1_ragged()), 1 << 20, es, 2)
+    hp = dict(lr=1e-2, momentum=0.9, wd=1e-4)
+    run = O.Run(plan, seed=3, dtype=dtype, opt="sgd", hp=hp)
+    for _ in range(4):
+        run.step()
+        for a, b in ((run.p, run.sp), (run.m, run.sm)):
+            np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+        assert not run.v.any() and not run.sv.any()
+    idx = np.random.default_rng(1).choice(plan.total, 3000, replace=False).astype(np.int64)
+    used = plan.used_mask()[idx]
+    p, b, R = O.run_sample_sgd(3, 2, dtype, 10, 4, idx, used, **hp)
+    np.testing.assert_array_equal(p, run.p[idx])
+    np.testing.assert_array_equal(b, run.m[idx])
