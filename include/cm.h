@@ -122,6 +122,13 @@ typedef struct {
     double lr, beta1, beta2, eps, weight_decay;
 } cm_adamw;
 
+/* SGD-with-momentum hyper-parameters for one step (SPEC.md:310-316
+ * [OP] sgd_step; PAPER.md:307 names SGD among the functional optimizers).  weight_decay
+ * != 0 adds the coupled L2 term to the gradient (reading R27); 0 gives the SPEC form. */
+typedef struct {
+    double lr, momentum, weight_decay;
+} cm_sgd;
+
 /* ------------------------------------------------------------------ planning (pure)
  * cm_plan_buckets -- the bucket plan, PAPER.md:258-264 (sec 4.2.2), reading R10-R13:
  * walk tensors from the last to the first; add a tensor to the open bucket while the
@@ -219,6 +226,18 @@ cm_status cm_allreduce_multicast(cm_ctx *ctx, int32_t bucket, int64_t iteration,
  * otherwise: "no partial update").  Records the step's scalars for the
  * shadow.  With CM_FLAG_NO_TAP the all-reduce has no tap and no shadow exists.        */
 cm_status cm_apply_step(cm_ctx *ctx, int64_t step, const cm_adamw *hp, void *stream);
+
+/* cm_apply_step_sgd -- the same step with SGD-momentum instead of AdamW (SPEC.md:310-316,
+ * reading R27), one fused HBM-bound kernel over the same flat buffers:
+ *   g = R*inv_n; d = g  (or g + wd*p when weight_decay != 0); buf = mu*buf + d;
+ *   p = p - lr*buf
+ * fp32 IEEE ops, no FMA.  The velocity buf lives in the m buffer; v is not read or
+ * written (keep it zero).  The step's optimizer kind and scalars go into the ring-slot
+ * record, so the shadow and restore roll-forward replay SGD with identical bits.  The
+ * first step of a context fixes its optimizer: switching between cm_apply_step and
+ * cm_apply_step_sgd later is CM_ERR_STATE.  Same preconditions and errors as
+ * cm_apply_step; works with CM_FLAG_ZERO1 (velocity shard-local).                    */
+cm_status cm_apply_step_sgd(cm_ctx *ctx, int64_t step, const cm_sgd *hp, void *stream);
 
 /* cm_shadow_apply -- the shadow replica's step `step` (Listing 2, PAPER.md:290-298:
  * "buckets.recv(); optimizer.step()"), enqueued on `side_stream`, off the training

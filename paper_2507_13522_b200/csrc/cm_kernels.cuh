@@ -316,6 +316,25 @@ __device__ __forceinline__ void adamw_elem(float R, const AdamScalars& s, float&
     v = vv;
 }
 
+// SGD with momentum (reading R27), fp32, no FMA:
+//   g = R*inv_n; d = g (wd_on = 0) or g + wd*p (wd_on = 1); buf = mu*buf + d; p = p - lr*buf
+// The velocity lives in the m array; v is not touched.
+struct SgdScalars {
+    float mu, inv_n, lr, wd;
+    int wd_on;
+};
+
+__device__ __forceinline__ void sgd_elem(float R, const SgdScalars& q, float& p, float& buf) {
+    const float g = __fmul_rn(R, q.inv_n);
+    const float d = q.wd_on ? __fadd_rn(g, __fmul_rn(q.wd, p)) : g;
+    const float b = __fadd_rn(__fmul_rn(q.mu, buf), d);
+    p = __fsub_rn(p, __fmul_rn(q.lr, b));
+    buf = b;
+}
+
+// Optimizer selector of the element-local step kernels (same data path, different op).
+enum OptKind : int { kOptAdamW = 0, kOptSgd = 1 };
+
 // A work item = 8 consecutive elements (two float4 of state; 32 B of fp32 grads or 16 B
 // of bf16 grads).  All arrays are 16-byte aligned and a multiple of 8 elements long
 // except possibly a 4-element tail for fp32 (handled by the tail item path).
@@ -326,10 +345,24 @@ struct AdamParams {
     float* p_out; float* m_out; float* v_out;
     int64_t n;          // elements (multiple of 4)
     AdamScalars s;
+    SgdScalars q;       // used by the kOptSgd instances (v_in / v_out unused there)
     volatile float* hp_rec;        // host-mapped ring-slot scalar record (or nullptr)
+    volatile int32_t* hp_kind;     // host-mapped record: optimizer kind
     volatile int64_t* hp_tag;      // written after the record: the step
+    float rec[10];                 // the record's scalars (AdamScalars or SgdScalars)
+    int32_t rec_kind;
     int64_t step;
 };
+
+// the step's scalars into the host-mapped ring-slot record, then its tag (one thread)
+template <typename PT>
+__device__ __forceinline__ void write_record(const PT& P) {
+    if (!P.hp_rec) return;
+    for (int k = 0; k < 10; ++k) P.hp_rec[k] = P.rec[k];
+    *P.hp_kind = P.rec_kind;
+    __threadfence_system();
+    *P.hp_tag = P.step;
+}
 
 constexpr int kAdamThreads = 256;
 
@@ -385,12 +418,7 @@ __global__ void __launch_bounds__(kAdamThreads) adamw_kernel(const AdamParams P)
             P.p_out[e] = p; P.m_out[e] = m; P.v_out[e] = v;
         }
     }
-    if (P.hp_rec && blockIdx.x == 0 && threadIdx.x == 0) {
-        const float* sf = &P.s.c1;
-        for (int k = 0; k < 10; ++k) P.hp_rec[k] = sf[k];
-        __threadfence_system();
-        *P.hp_tag = P.step;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) write_record(P);
 }
 
 // ------------------------------------------------------------------ AdamW, warp-tiled
@@ -400,7 +428,7 @@ __global__ void __launch_bounds__(kAdamThreads) adamw_kernel(const AdamParams P)
 // either is stored (16 independent 16-byte loads in flight per thread).
 constexpr int kWarpTile = 256;
 
-template <typename G>
+template <typename G, int OPT = kOptAdamW>
 __device__ __forceinline__ void wt_load(const AdamParams& P, int64_t e, float4& g, float4& p, float4& m, float4& v) {
     if constexpr (std::is_same<G, F32Tag>::value) {
         g = __ldcs(reinterpret_cast<const float4*>((const float*)P.g + e));
@@ -410,21 +438,29 @@ __device__ __forceinline__ void wt_load(const AdamParams& P, int64_t e, float4& 
     }
     p = __ldcs(reinterpret_cast<const float4*>(P.p_in + e));
     m = __ldcs(reinterpret_cast<const float4*>(P.m_in + e));
-    v = __ldcs(reinterpret_cast<const float4*>(P.v_in + e));
+    if constexpr (OPT == kOptAdamW) v = __ldcs(reinterpret_cast<const float4*>(P.v_in + e));
 }
+template <int OPT = kOptAdamW>
 __device__ __forceinline__ void wt_compute_store(const AdamParams& P, int64_t e, const float4& g, float4 p,
                                                  float4 m, float4 v) {
-    adamw_elem(g.x, P.s, p.x, m.x, v.x);
-    adamw_elem(g.y, P.s, p.y, m.y, v.y);
-    adamw_elem(g.z, P.s, p.z, m.z, v.z);
-    adamw_elem(g.w, P.s, p.w, m.w, v.w);
+    if constexpr (OPT == kOptAdamW) {
+        adamw_elem(g.x, P.s, p.x, m.x, v.x);
+        adamw_elem(g.y, P.s, p.y, m.y, v.y);
+        adamw_elem(g.z, P.s, p.z, m.z, v.z);
+        adamw_elem(g.w, P.s, p.w, m.w, v.w);
+    } else {
+        sgd_elem(g.x, P.q, p.x, m.x);
+        sgd_elem(g.y, P.q, p.y, m.y);
+        sgd_elem(g.z, P.q, p.z, m.z);
+        sgd_elem(g.w, P.q, p.w, m.w);
+    }
     __stcs(reinterpret_cast<float4*>(P.p_out + e), p);
     __stcs(reinterpret_cast<float4*>(P.m_out + e), m);
-    __stcs(reinterpret_cast<float4*>(P.v_out + e), v);
+    if constexpr (OPT == kOptAdamW) __stcs(reinterpret_cast<float4*>(P.v_out + e), v);
 }
 
-template <typename G>
-__global__ void __launch_bounds__(kAdamThreads) adamw_wt_kernel(const AdamParams P) {
+template <typename G, int OPT>
+__device__ __forceinline__ void wt_body(const AdamParams& P) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)kAdamThreads + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kAdamThreads) >> 5;
@@ -433,39 +469,45 @@ __global__ void __launch_bounds__(kAdamThreads) adamw_wt_kernel(const AdamParams
     for (; t + nwarps < tiles; t += 2 * nwarps) {
         const int64_t a0 = t * kWarpTile + 4 * lane, a1 = a0 + 128;
         const int64_t b0 = (t + nwarps) * kWarpTile + 4 * lane, b1 = b0 + 128;
-        float4 g[4], p[4], m[4], v[4];
-        wt_load<G>(P, a0, g[0], p[0], m[0], v[0]);
-        wt_load<G>(P, a1, g[1], p[1], m[1], v[1]);
-        wt_load<G>(P, b0, g[2], p[2], m[2], v[2]);
-        wt_load<G>(P, b1, g[3], p[3], m[3], v[3]);
-        wt_compute_store(P, a0, g[0], p[0], m[0], v[0]);
-        wt_compute_store(P, a1, g[1], p[1], m[1], v[1]);
-        wt_compute_store(P, b0, g[2], p[2], m[2], v[2]);
-        wt_compute_store(P, b1, g[3], p[3], m[3], v[3]);
+        float4 g[4], p[4], m[4], v[4] = {};
+        wt_load<G, OPT>(P, a0, g[0], p[0], m[0], v[0]);
+        wt_load<G, OPT>(P, a1, g[1], p[1], m[1], v[1]);
+        wt_load<G, OPT>(P, b0, g[2], p[2], m[2], v[2]);
+        wt_load<G, OPT>(P, b1, g[3], p[3], m[3], v[3]);
+        wt_compute_store<OPT>(P, a0, g[0], p[0], m[0], v[0]);
+        wt_compute_store<OPT>(P, a1, g[1], p[1], m[1], v[1]);
+        wt_compute_store<OPT>(P, b0, g[2], p[2], m[2], v[2]);
+        wt_compute_store<OPT>(P, b1, g[3], p[3], m[3], v[3]);
     }
     for (; t < tiles; t += nwarps) {
         const int64_t a0 = t * kWarpTile + 4 * lane, a1 = a0 + 128;
-        float4 g[2], p[2], m[2], v[2];
-        wt_load<G>(P, a0, g[0], p[0], m[0], v[0]);
-        wt_load<G>(P, a1, g[1], p[1], m[1], v[1]);
-        wt_compute_store(P, a0, g[0], p[0], m[0], v[0]);
-        wt_compute_store(P, a1, g[1], p[1], m[1], v[1]);
+        float4 g[2], p[2], m[2], v[2] = {};
+        wt_load<G, OPT>(P, a0, g[0], p[0], m[0], v[0]);
+        wt_load<G, OPT>(P, a1, g[1], p[1], m[1], v[1]);
+        wt_compute_store<OPT>(P, a0, g[0], p[0], m[0], v[0]);
+        wt_compute_store<OPT>(P, a1, g[1], p[1], m[1], v[1]);
     }
     // tail: n % 256 elements (a multiple of 4), one float4 group per thread of block 0
     if (blockIdx.x == 0) {
         const int64_t e = tiles * kWarpTile + 4 * (int64_t)threadIdx.x;
         if (e < P.n) {
-            float4 g, p, m, v;
-            wt_load<G>(P, e, g, p, m, v);
-            wt_compute_store(P, e, g, p, m, v);
+            float4 g, p, m, v = {};
+            wt_load<G, OPT>(P, e, g, p, m, v);
+            wt_compute_store<OPT>(P, e, g, p, m, v);
         }
     }
-    if (P.hp_rec && blockIdx.x == 0 && threadIdx.x == 0) {
-        const float* sf = &P.s.c1;
-        for (int k = 0; k < 10; ++k) P.hp_rec[k] = sf[k];
-        __threadfence_system();
-        *P.hp_tag = P.step;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) write_record(P);
+}
+
+template <typename G>
+__global__ void __launch_bounds__(kAdamThreads) adamw_wt_kernel(const AdamParams P) {
+    wt_body<G, kOptAdamW>(P);
+}
+
+// SGD-momentum over the same warp tiles: HBM sizeof(G) + 8 read + 8 write B/elem
+template <typename G>
+__global__ void __launch_bounds__(kAdamThreads) sgd_wt_kernel(const AdamParams P) {
+    wt_body<G, kOptSgd>(P);
 }
 
 // ------------------------------------------------------------------ AdamW, TMA-staged
@@ -593,12 +635,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adamw_tma_kernel(const AdamPar
         }
     }
     if (leader) bulk_wait0();
-    if (P.hp_rec && blockIdx.x == 0 && threadIdx.x == 0) {
-        const float* sf = &P.s.c1;
-        for (int k = 0; k < 10; ++k) P.hp_rec[k] = sf[k];
-        __threadfence_system();
-        *P.hp_tag = P.step;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) write_record(P);
 }
 
 // ------------------------------------------------------------------ ZeRO-1: AdamW + AG
@@ -617,14 +654,18 @@ struct Zero1Params {
     int nb, n, rank, barriers;
     int64_t L;                      // shard elements
     AdamScalars s;
+    SgdScalars q;
     Pads pads;
     uint32_t epoch;
     volatile float* hp_rec;
+    volatile int32_t* hp_kind;
     volatile int64_t* hp_tag;
+    float rec[10];
+    int32_t rec_kind;
     int64_t step;
 };
 
-template <typename G, int N>
+template <typename G, int N, int OPT = kOptAdamW>
 __global__ void __launch_bounds__(256) adamw_zero1_kernel(const Zero1Params P) {
     int b = 0;
     const int64_t groups = P.L / 4;
@@ -643,24 +684,26 @@ __global__ void __launch_bounds__(256) adamw_zero1_kernel(const Zero1Params P) {
         }
         float4 p = __ldcs(reinterpret_cast<const float4*>(P.p[P.rank] + flat));
         float4 m = __ldcs(reinterpret_cast<const float4*>(P.m + j));
-        float4 v = __ldcs(reinterpret_cast<const float4*>(P.v + j));
-        adamw_elem(g.x, P.s, p.x, m.x, v.x);
-        adamw_elem(g.y, P.s, p.y, m.y, v.y);
-        adamw_elem(g.z, P.s, p.z, m.z, v.z);
-        adamw_elem(g.w, P.s, p.w, m.w, v.w);
+        if constexpr (OPT == kOptAdamW) {
+            float4 v = __ldcs(reinterpret_cast<const float4*>(P.v + j));
+            adamw_elem(g.x, P.s, p.x, m.x, v.x);
+            adamw_elem(g.y, P.s, p.y, m.y, v.y);
+            adamw_elem(g.z, P.s, p.z, m.z, v.z);
+            adamw_elem(g.w, P.s, p.w, m.w, v.w);
+            __stcs(reinterpret_cast<float4*>(P.v + j), v);
+        } else {
+            sgd_elem(g.x, P.q, p.x, m.x);
+            sgd_elem(g.y, P.q, p.y, m.y);
+            sgd_elem(g.z, P.q, p.z, m.z);
+            sgd_elem(g.w, P.q, p.w, m.w);
+        }
         __stcs(reinterpret_cast<float4*>(P.m + j), m);
-        __stcs(reinterpret_cast<float4*>(P.v + j), v);
         const uint4 pw = make_uint4(__float_as_uint(p.x), __float_as_uint(p.y), __float_as_uint(p.z),
                                     __float_as_uint(p.w));
 #pragma unroll
         for (int k = 0; k < N; ++k) st_v4(P.p[k] + flat, pw);   // own p + all-gather
     }
-    if (P.hp_rec && blockIdx.x == 0 && threadIdx.x == 0) {
-        const float* sf = &P.s.c1;
-        for (int k = 0; k < 10; ++k) P.hp_rec[k] = sf[k];
-        __threadfence_system();
-        *P.hp_tag = P.step;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) write_record(P);
     if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 1);   // every shard landed everywhere
 }
 

@@ -57,8 +57,9 @@ static_assert(sizeof(SegHeader) <= kAlign, "header");
 
 struct SlotMeta {
     volatile int64_t step_tag;  // step whose scalars follow (written after them)
-    volatile float sc[10];
-    int32_t pad[4];
+    volatile float sc[10];      // AdamScalars (kind 0) or SgdScalars (kind 1)
+    volatile int32_t kind;      // OptKind of the step
+    int32_t pad[3];
 };
 static_assert(sizeof(SlotMeta) == 64, "meta");
 
@@ -93,6 +94,27 @@ struct Blob {
 };
 
 typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+// One step's optimizer and scalars: what the trainer used, what the shadow and the
+// restore roll-forward replay (the ring-slot record holds the same ten floats + kind).
+struct StepRec {
+    int kind = kOptAdamW;
+    AdamScalars a{};
+    SgdScalars q{};
+    void to_floats(float* f) const {
+        memset(f, 0, 10 * sizeof(float));
+        if (kind == kOptAdamW) memcpy(f, &a, sizeof a);
+        else { f[0] = q.mu; f[1] = q.inv_n; f[2] = q.lr; f[3] = q.wd; f[4] = q.wd_on ? 1.0f : 0.0f; }
+    }
+    static StepRec from_floats(int kind, const float* f) {
+        StepRec r;
+        r.kind = kind;
+        if (kind == kOptAdamW) memcpy(&r.a, f, sizeof r.a);
+        else { r.q.mu = f[0]; r.q.inv_n = f[1]; r.q.lr = f[2]; r.q.wd = f[3]; r.q.wd_on = f[4] != 0.0f; }
+        return r;
+    }
+};
+static_assert(sizeof(AdamScalars) == 10 * sizeof(float), "record");
 
 }  // namespace
 
@@ -170,7 +192,8 @@ struct cm_ctx {
     int K = 1;                       // persist the host snapshot every K shadow steps
     int64_t released_upto = 0;       // ring slots of iterations < released_upto are free
     int64_t hh_step[2] = {0, -1};    // host snapshot halves' steps (enqueue-time mirror)
-    std::vector<AdamScalars> slot_sc;
+    int opt_kind = -1;               // optimizer fixed by the first step (-1: none yet)
+    std::vector<StepRec> slot_sc;
     std::vector<int64_t> slot_sc_step;
     std::vector<cudaEvent_t> ev_tap_done, ev_slot_free;
 
@@ -296,6 +319,17 @@ static AdamScalars make_scalars(cm_ctx* c, int64_t s, const cm_adamw& hp) {
     return a;
 }
 
+// SGD-momentum scalars (reading R27): fp64 -> fp32 once; wd_on decided on the host
+static SgdScalars make_sgd_scalars(cm_ctx* c, const cm_sgd& hp) {
+    SgdScalars q;
+    q.mu = (float)hp.momentum;
+    q.inv_n = (float)(1.0 / (double)c->n);
+    q.lr = (float)hp.lr;
+    q.wd = (float)hp.weight_decay;
+    q.wd_on = hp.weight_decay != 0.0 ? 1 : 0;
+    return q;
+}
+
 // ---------------------------------------------------------------- launch helpers
 template <typename G, int N>
 static int ar_occ_n() {
@@ -334,7 +368,14 @@ static void launch_ar_t(int n, dim3 grid, cudaStream_t s, const ArParams& P) {
 }
 
 static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaStream_t s) {
-    if (c->adamw_impl == 1) {
+    if (P.rec_kind == kOptSgd) {
+        // SGD-momentum: the warp-tiled data path only
+        const int64_t tiles = P.n / kWarpTile;
+        const int64_t want = std::max<int64_t>(1, (tiles + kAdamThreads / 32 - 1) / (kAdamThreads / 32));
+        const int grid = (int)std::min<int64_t>(want, std::min(blocks, c->wt_blocks));
+        if (c->dtype == CM_F32) sgd_wt_kernel<F32Tag><<<grid, kAdamThreads, 0, s>>>(P);
+        else sgd_wt_kernel<BF16Tag><<<grid, kAdamThreads, 0, s>>>(P);
+    } else if (c->adamw_impl == 1) {
         const int64_t tiles = (P.n + kTmaTile - 1) / kTmaTile;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->tma_blocks));
         if (c->dtype == CM_F32)
@@ -359,22 +400,35 @@ static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaSt
     return CM_OK;
 }
 
-template <typename G>
+template <typename G, int OPT>
 static void launch_zero1_t(int n, int grid, cudaStream_t s, const Zero1Params& Z) {
     switch (n) {
-        case 1: adamw_zero1_kernel<G, 1><<<grid, 256, 0, s>>>(Z); break;
-        case 2: adamw_zero1_kernel<G, 2><<<grid, 256, 0, s>>>(Z); break;
-        case 3: adamw_zero1_kernel<G, 3><<<grid, 256, 0, s>>>(Z); break;
-        case 4: adamw_zero1_kernel<G, 4><<<grid, 256, 0, s>>>(Z); break;
-        case 5: adamw_zero1_kernel<G, 5><<<grid, 256, 0, s>>>(Z); break;
-        case 6: adamw_zero1_kernel<G, 6><<<grid, 256, 0, s>>>(Z); break;
-        case 7: adamw_zero1_kernel<G, 7><<<grid, 256, 0, s>>>(Z); break;
-        default: adamw_zero1_kernel<G, 8><<<grid, 256, 0, s>>>(Z); break;
+        case 1: adamw_zero1_kernel<G, 1, OPT><<<grid, 256, 0, s>>>(Z); break;
+        case 2: adamw_zero1_kernel<G, 2, OPT><<<grid, 256, 0, s>>>(Z); break;
+        case 3: adamw_zero1_kernel<G, 3, OPT><<<grid, 256, 0, s>>>(Z); break;
+        case 4: adamw_zero1_kernel<G, 4, OPT><<<grid, 256, 0, s>>>(Z); break;
+        case 5: adamw_zero1_kernel<G, 5, OPT><<<grid, 256, 0, s>>>(Z); break;
+        case 6: adamw_zero1_kernel<G, 6, OPT><<<grid, 256, 0, s>>>(Z); break;
+        case 7: adamw_zero1_kernel<G, 7, OPT><<<grid, 256, 0, s>>>(Z); break;
+        default: adamw_zero1_kernel<G, 8, OPT><<<grid, 256, 0, s>>>(Z); break;
     }
 }
 static void launch_zero1(cm_ctx* c, const Zero1Params& Z, int grid, cudaStream_t s) {
-    if (c->dtype == CM_F32) launch_zero1_t<F32Tag>(c->n, grid, s, Z);
-    else launch_zero1_t<BF16Tag>(c->n, grid, s, Z);
+    if (Z.rec_kind == kOptSgd) {
+        if (c->dtype == CM_F32) launch_zero1_t<F32Tag, kOptSgd>(c->n, grid, s, Z);
+        else launch_zero1_t<BF16Tag, kOptSgd>(c->n, grid, s, Z);
+    } else {
+        if (c->dtype == CM_F32) launch_zero1_t<F32Tag, kOptAdamW>(c->n, grid, s, Z);
+        else launch_zero1_t<BF16Tag, kOptAdamW>(c->n, grid, s, Z);
+    }
+}
+
+// the params of one element-local step kernel for record r
+static void set_step(AdamParams& P, const StepRec& r) {
+    P.s = r.a;
+    P.q = r.q;
+    P.rec_kind = r.kind;
+    r.to_floats(P.rec);
 }
 
 static cm_status publish(cm_ctx* c, volatile int64_t* host_field, int64_t value, cudaStream_t s) {
@@ -559,7 +613,7 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
         c->ev_tap_done.push_back(a);
         c->ev_slot_free.push_back(b);
     }
-    c->slot_sc.assign(c->D, AdamScalars{});
+    c->slot_sc.assign(c->D, StepRec{});
     c->slot_sc_step.assign(c->D, -1);
     return CM_OK;
 }
@@ -815,6 +869,7 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
         return fail(c, CM_ERR_STATE, "DEVICE-placed shadow cannot be attached after a restart");
     }
     CU(cudaMalloc(&c->state_dev_alloc, 6 * (size_t)c->shard_numel * 4));
+    CU(cudaMemset(c->state_dev_alloc, 0, 6 * (size_t)c->shard_numel * 4));
     for (int hf = 0; hf < 2; ++hf)
         for (int a = 0; a < 3; ++a) c->sd[hf][a] = c->state_dev_alloc + ((size_t)hf * 3 + a) * c->shard_numel;
     if (!c->attach) {
@@ -953,27 +1008,55 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     return CM_OK;
 }
 
-cm_status cm_apply_step(cm_ctx* c, int64_t step, const cm_adamw* hp, void* stream) {
-    if (!c || !hp) return CM_ERR_ARG;
+static cm_status step_checks(cm_ctx* c, int64_t step, int kind) {
     if (c->cuda_dead) return CM_ERR_CUDA;
     if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
     if (step != c->train_step + 1) return fail(c, CM_ERR_STATE, "step %lld follows %lld", (long long)step, (long long)c->train_step);
     if (c->cur_iter != step - 1 || c->issued_count != (int)c->buckets.size())
         return fail(c, CM_ERR_STATE, "step %lld before all buckets of iteration %lld were all-reduced (%d/%zu)",
                     (long long)step, (long long)(step - 1), c->issued_count, c->buckets.size());
-    const AdamScalars a = make_scalars(c, step, *hp);
+    if (c->opt_kind >= 0 && c->opt_kind != kind)
+        return fail(c, CM_ERR_STATE, "optimizer changed mid-run (%s after %s steps): m/v would change meaning",
+                    kind == kOptSgd ? "SGD" : "AdamW", c->opt_kind == kOptSgd ? "SGD" : "AdamW");
+    return CM_OK;
+}
+
+static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* stream);
+
+cm_status cm_apply_step(cm_ctx* c, int64_t step, const cm_adamw* hp, void* stream) {
+    if (!c || !hp) return CM_ERR_ARG;
+    cm_status st = step_checks(c, step, kOptAdamW);
+    if (st != CM_OK) return st;
+    StepRec r;
+    r.kind = kOptAdamW;
+    r.a = make_scalars(c, step, *hp);
+    return apply_impl(c, step, r, stream);
+}
+
+cm_status cm_apply_step_sgd(cm_ctx* c, int64_t step, const cm_sgd* hp, void* stream) {
+    if (!c || !hp) return CM_ERR_ARG;
+    cm_status st = step_checks(c, step, kOptSgd);
+    if (st != CM_OK) return st;
+    StepRec r;
+    r.kind = kOptSgd;
+    r.q = make_sgd_scalars(c, *hp);
+    return apply_impl(c, step, r, stream);
+}
+
+static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* stream) {
     const int slot = (int)((step - 1) % c->D);
-    c->slot_sc[slot] = a;
+    c->slot_sc[slot] = rec;
     c->slot_sc_step[slot] = step;
     AdamParams P{};
     P.g = c->grad;
     P.p_in = c->p; P.m_in = c->m; P.v_in = c->v;
     P.p_out = c->p; P.m_out = c->m; P.v_out = c->v;
     P.n = c->P_pad;
-    P.s = a;
+    set_step(P, rec);
     if (!c->no_tap) {
         SlotMeta* sm = slot_meta(c, slot);
         P.hp_rec = to_dev(c, sm->sc);
+        P.hp_kind = to_dev(c, &sm->kind);
         P.hp_tag = to_dev(c, &sm->step_tag);
         P.step = step;
     }
@@ -989,10 +1072,13 @@ cm_status cm_apply_step(cm_ctx* c, int64_t step, const cm_adamw* hp, void* strea
         Z.nb = (int)c->buckets.size();
         Z.n = c->n; Z.rank = c->rank; Z.barriers = c->barriers ? 1 : 0;
         Z.L = c->shard_numel;
-        Z.s = a;
+        Z.s = P.s;
+        Z.q = P.q;
         Z.pads = c->pads;
         Z.epoch = ++c->epoch;
-        Z.hp_rec = P.hp_rec; Z.hp_tag = P.hp_tag; Z.step = step;
+        Z.hp_rec = P.hp_rec; Z.hp_kind = P.hp_kind; Z.hp_tag = P.hp_tag; Z.step = step;
+        memcpy(Z.rec, P.rec, sizeof Z.rec);
+        Z.rec_kind = P.rec_kind;
         const int64_t want = (Z.L / 4 + 255) / 256;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c->zero1_blocks));
         {
@@ -1010,6 +1096,7 @@ cm_status cm_apply_step(cm_ctx* c, int64_t step, const cm_adamw* hp, void* strea
     if (!c->no_tap && c->ce_tap)   // the caller may overwrite grads after this: taps first
         CU(cudaStreamWaitEvent(S(stream), c->ev_tap_done[slot], 0));
     c->train_step = step;
+    c->opt_kind = rec.kind;
     return CM_OK;
 }
 
@@ -1045,7 +1132,7 @@ static cm_status ensure_staging(cm_ctx* c) {
 // when step % K == 0 (or when forced): the host then holds a snapshot plus the tapped
 // gradients since it -- every step remains recoverable from host memory alone (restore
 // rolls forward over the ring), with 12/K instead of 12 bytes per element of D2H.
-static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars& a, cudaStream_t s,
+static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec, cudaStream_t s,
                                      bool force_persist, bool* persisted, const char* dev_g = nullptr) {
     const int slot = (int)((step - 1) % c->D);
     const int hin = (int)((step - 1) & 1), hout = (int)(step & 1);
@@ -1086,7 +1173,7 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars&
             AdamParams P{};
             P.g = dev_g ? (const void*)(dev_g + lo * c->es) : (const void*)c->stg_g[j];
             P.n = len;
-            P.s = a;
+            set_step(P, rec);
             P.p_in = c->sd[hin][0] + lo; P.m_in = c->sd[hin][1] + lo; P.v_in = c->sd[hin][2] + lo;
             P.p_out = c->sd[hout][0] + lo; P.m_out = c->sd[hout][1] + lo; P.v_out = c->sd[hout][2] + lo;
             st = launch_adamw(c, P, c->shadow_blocks, c->cs_k);
@@ -1094,7 +1181,8 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const AdamScalars&
             CU(cudaEventRecord(c->ev_stg_free[j], c->cs_k));
             if (persist) {   // copy engine D2H of the new state chunk into the host snapshot half
                 CU(cudaStreamWaitEvent(c->cs_d2h, c->ev_stg_free[j], 0));
-                for (int k = 0; k < 3; ++k)
+                // SGD leaves v untouched (all zero in every half): p and the velocity only
+                for (int k = 0; k < (rec.kind == kOptSgd ? 2 : 3); ++k)
                     CU(cudaMemcpyAsync(c->sh[ph][k] + lo, c->sd[hout][k] + lo, (size_t)len * 4,
                                        cudaMemcpyDeviceToHost, c->cs_d2h));
             }
@@ -1343,9 +1431,10 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     for (int64_t st = b + 1; st <= I; ++st) {   // roll forward over the ring
         const int slot = (int)((st - 1) % c->D);
         const SlotMeta* sm = slot_meta(c, slot);
-        AdamScalars a;
-        memcpy(&a, (const void*)sm->sc, sizeof a);
-        cm_status r = shadow_step_enqueue(c, st, a, s, /*force_persist=*/st == I, nullptr);
+        float f[10];
+        for (int k = 0; k < 10; ++k) f[k] = sm->sc[k];
+        const StepRec rec = StepRec::from_floats(sm->kind, f);
+        cm_status r = shadow_step_enqueue(c, st, rec, s, /*force_persist=*/st == I, nullptr);
         if (r != CM_OK) return r;
     }
     c->hdr->shadow_step = I;

@@ -58,10 +58,11 @@ class VirtualGroup:
 
     def __init__(self, numel, world_size, device=0, grad_dtype=cm.CM_F32, cap_bytes=W.CAP_BYTES,
                  shm_name="cmvg", ring_depth=2, shadow_place=cm.CM_SHADOW_HOST, flags=0, seed=W.SEED,
-                 gscale=W.GRAD_SCALE, hp=None, persist_every=1):
+                 gscale=W.GRAD_SCALE, hp=None, persist_every=1, opt="adamw"):
         self.n = world_size
         self.seed, self.gscale = seed, gscale
-        self.hp = dict(W.HP)
+        self.opt = opt
+        self.hp = dict(W.HP_SGD if opt == "sgd" else W.HP)
         if hp:
             self.hp.update(hp)
         self.no_tap = bool(flags & cm.CM_FLAG_NO_TAP)
@@ -90,7 +91,10 @@ class VirtualGroup:
     def apply(self, step=None):
         step = self.t + 1 if step is None else step
         for r in self.ranks:
-            r.ctx.apply_step(step, stream=self.stream, **self.hp)
+            if self.opt == "sgd":
+                r.ctx.apply_step_sgd(step, stream=self.stream, **self.hp)
+            else:
+                r.ctx.apply_step(step, stream=self.stream, **self.hp)
 
     def shadow(self, step=None):
         step = self.t + 1 if step is None else step
@@ -121,14 +125,15 @@ class DistRank:
 
     def __init__(self, numel, grad_dtype=cm.CM_F32, cap_bytes=W.CAP_BYTES, shm_name="cmdist", ring_depth=2,
                  shadow_place=cm.CM_SHADOW_HOST, flags=0, seed=W.SEED, gscale=W.GRAD_SCALE, hp=None,
-                 persist_every=1):
+                 persist_every=1, opt="adamw"):
         import torch.distributed as dist
         self.n = dist.get_world_size()
         self.rank_id = dist.get_rank()
         local = int(os.environ.get("LOCAL_RANK", self.rank_id))
         torch.cuda.set_device(local)
         self.seed, self.gscale = seed, gscale
-        self.hp = dict(W.HP)
+        self.opt = opt
+        self.hp = dict(W.HP_SGD if opt == "sgd" else W.HP)
         if hp:
             self.hp.update(hp)
         self.no_tap = bool(flags & cm.CM_FLAG_NO_TAP)
@@ -149,7 +154,10 @@ class DistRank:
             c.gen_grads(self.seed, self.t, self.gscale, self.stream)
         for b in range(self.n_buckets):
             c.allreduce_multicast(b, self.t, self.stream)
-        c.apply_step(self.t + 1, stream=self.stream, **self.hp)
+        if self.opt == "sgd":
+            c.apply_step_sgd(self.t + 1, stream=self.stream, **self.hp)
+        else:
+            c.apply_step(self.t + 1, stream=self.stream, **self.hp)
         if shadow and not self.no_tap:
             c.shadow_apply(self.t + 1, self.side)
         self.t += 1

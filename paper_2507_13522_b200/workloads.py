@@ -11,6 +11,7 @@ SEED = 0
 GRAD_SCALE = 10          # s: gradients are int-mantissa * 2^(-23-e-s) (fp32) / 2^(-7-e-s) (bf16)
 CAP_BYTES = 25 << 20     # PyTorch DDP default bucket cap, 25 MiB (reading R11)
 HP = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)   # SPEC.md:342 defaults
+HP_SGD = dict(lr=1e-2, momentum=0.9, weight_decay=1e-4)   # SGD-momentum (f4, reading R27)
 
 
 def gpt2_small():

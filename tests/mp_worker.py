@@ -3,7 +3,7 @@ torch.distributed.run from tests/test_gpu_multiproc.py).  Each rank runs the hot
 real NVLink peer memory and checks its own state bit-for-bit against the oracle.
 
   python -m torch.distributed.run --nproc-per-node N tests/mp_worker.py <mode> <name>
-modes: parity_f32, parity_bf16, restore_soft, hardkill_phase1, hardkill_phase2
+modes: parity_f32, parity_bf16, parity_zero1, parity_sgd, restore_soft, hardkill_phase1, hardkill_phase2
 """
 import os
 import sys
@@ -63,11 +63,14 @@ def main():
     numel = W.numels(W.c1_ragged()) + [5, 70001]
     cap = 1 << 20
     plan = O.Plan(numel, cap, 4 if dtype == cm.CM_F32 else 2, n)
-    ref = O.Run(plan, seed=0, dtype=dtype, gscale=W.GRAD_SCALE, hp=HP_O)
+    opt = "sgd" if mode == "parity_sgd" else "adamw"
+    hp_o = dict(lr=W.HP_SGD["lr"], momentum=W.HP_SGD["momentum"], wd=W.HP_SGD["weight_decay"]) \
+        if opt == "sgd" else HP_O
+    ref = O.Run(plan, seed=0, dtype=dtype, gscale=W.GRAD_SCALE, hp=hp_o, opt=opt)
     flags = cm.CM_FLAG_ATTACH if mode == "hardkill_phase2" else 0
     if mode == "parity_zero1":
         flags |= cm.CM_FLAG_ZERO1
-    R = harness.DistRank(numel, dtype, cap, name, 2, cm.CM_SHADOW_HOST, flags)
+    R = harness.DistRank(numel, dtype, cap, name, 2, cm.CM_SHADOW_HOST, flags, opt=opt)
     if mode.startswith("parity"):
         for t in range(6):
             R.step()
