@@ -295,6 +295,68 @@ __global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P)
     if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 1);   // bucket complete everywhere
 }
 
+// ------------------------------------------------------------------ one-shot push AR
+// small buckets (Llama's 16 KiB norm pairs) are latency-bound, and the
+// two-shot kernel pays a pull round trip over NVLink plus an exit barrier for the remote
+// all-gather stores.  One-shot push: every rank stores its whole bucket into slot [rank] of
+// every peer's inbox (posted NVLink writes), one pairwise block barrier, then every rank
+// sums all n copies in rank order from its LOCAL inbox (identical R on every rank: same
+// operands, same order) and writes its own grad buffer only.  Rank r taps only the
+// elements of its own shard, so the tap stays exactly once box-wide.  Traffic per GPU is
+// (n-1) S_b each way instead of 2(n-1)/n S_b: only worth it where latency dominates.
+// Inbox halves alternate with the launch epoch; between two launches that use the same
+// half every rank has passed a barrier of the launch in between, so a slot is never
+// overwritten while its owner still reads it.
+struct OsParams {
+    char* own;                     // this rank's grad buffer + bucket byte offset
+    char* push[kMaxRanks];         // peer k's inbox slot [rank] (unused for k == rank)
+    const char* inbox[kMaxRanks];  // this rank's inbox slot [k] (unused for k == rank)
+    char* tap;                     // tap target of this rank's shard (nullptr: no tap)
+    int64_t nvec;                  // 16-byte vectors in the bucket
+    int64_t shard_lo, shard_hi;    // this rank's shard, in vectors
+    Pads pads;
+    uint32_t epoch;
+    int rank;
+    unsigned long long* done_ctr;
+    unsigned long long done_target;
+    volatile uint64_t* tap_flag;
+    uint64_t tap_flag_value;
+};
+
+constexpr int kOsThreads = 256;
+
+template <typename G, int N>
+__global__ void __launch_bounds__(kOsThreads) os_tap_kernel(const OsParams P) {
+    const int64_t stride = (int64_t)gridDim.x * kOsThreads;
+    const int64_t q0 = blockIdx.x * (int64_t)kOsThreads + threadIdx.x;
+    for (int64_t q = q0; q < P.nvec; q += stride) {          // push
+        const uint4 x = ld_v4(P.own + q * 16);
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if (k != P.rank) st_v4(P.push[k] + q * 16, x);
+    }
+    block_barrier(P.pads, N, P.rank, P.epoch, 0);            // every rank's chunk arrived
+    for (int64_t q = q0; q < P.nvec; q += stride) {          // reduce from the local inbox
+        uint4 x[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) x[k] = ld_v4((k == P.rank ? (const char*)P.own : P.inbox[k]) + q * 16);
+        const uint4 r = reduce_vec<G, N>(x);
+        st_v4(P.own + q * 16, r);
+        if (P.tap && q >= P.shard_lo && q < P.shard_hi) st_cs_v4(P.tap + (q - P.shard_lo) * 16, r);
+    }
+    if (P.tap_flag) {
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long prev = atomicAdd(P.done_ctr, 1ull);
+            if (prev + 1 == P.done_target) {
+                __threadfence_system();
+                *P.tap_flag = P.tap_flag_value;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ AdamW
 // Canonical fp32 op sequence (reading R4), each op IEEE round-to-nearest, no FMA:
 //   g = R*inv_n; m = B1*m + c1*g; v = B2*v + c2*(g*g); mh = m/bc1; vh = v/bc2;
@@ -772,6 +834,13 @@ __global__ void __launch_bounds__(256) compare_kernel(const float* __restrict__ 
 __global__ void publish_kernel(volatile int64_t* dst, int64_t value) {
     __threadfence_system();
     *dst = value;
+    __threadfence_system();
+}
+
+// the same for `count` consecutive tap flags (one coalesced drain of several buckets)
+__global__ void publish_range_kernel(volatile uint64_t* dst, int count, uint64_t value) {
+    __threadfence_system();
+    for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = value;
     __threadfence_system();
 }
 

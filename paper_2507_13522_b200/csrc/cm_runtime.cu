@@ -41,6 +41,8 @@ constexpr uint64_t kMagic = 0x434B4D5442323030ull;  // "CKMTB200"
 constexpr uint32_t kVersion = 1;
 constexpr size_t kAlign = 4096;
 constexpr int kStages = 4;                       // shadow staging buffers
+constexpr int64_t kOsSlotBytes = 1ll << 20;      // one-shot inbox slot (largest one-shot bucket)
+constexpr int64_t kDrainCoalesce = 4ll << 20;    // tap drains of adjacent small shards merge up to this
 constexpr int64_t kStageElems = 8ll << 20;       // elements per shadow staging chunk
 
 struct SegHeader {
@@ -86,11 +88,11 @@ struct Blob {
     int32_t world_size, rank, device, dtype;
     uint64_t layout_hash;
     int64_t padded_numel;
-    // 0 grad, 1 p, 2 m, 3 v, 4 signal pad
-    cudaIpcMemHandle_t handle[5];
-    uint64_t base[5];       // allocation base address in the owner (dedupe key)
-    uint64_t offset[5];     // pointer - base
-    uint64_t raw[5];        // raw pointer (usable in-process)
+    // 0 grad, 1 p, 2 m, 3 v, 4 signal pad, 5 one-shot inbox
+    cudaIpcMemHandle_t handle[6];
+    uint64_t base[6];       // allocation base address in the owner (dedupe key)
+    uint64_t offset[6];     // pointer - base
+    uint64_t raw[6];        // raw pointer (usable in-process)
 };
 
 typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
@@ -149,6 +151,9 @@ struct cm_ctx {
     void* grad = nullptr;
     float *p = nullptr, *m = nullptr, *v = nullptr;
     uint32_t* pad = nullptr;
+    char* inbox = nullptr;                // one-shot inbox: 2 halves x n slots x kOsSlotBytes
+    char* peer_inbox[kMaxRanks] = {};
+    int64_t oneshot_max = 0;              // buckets <= this many bytes use the one-shot kernel
     char* peer_grad[kMaxRanks] = {};
     float* peer_p[kMaxRanks] = {};
     float* peer_m[kMaxRanks] = {};
@@ -202,6 +207,13 @@ struct cm_ctx {
     int64_t pw_s = 0;
 
     int64_t launches = 0;
+
+    // pending (not yet issued) copy-engine drain of adjacent tapped shards [dr_b0, dr_b1]
+    int dr_b0 = -1, dr_b1 = -1;
+    int64_t dr_iter = -1;
+    const char* dr_src = nullptr;
+    char* dr_dst = nullptr;
+    size_t dr_bytes = 0;
 
     // copy-engine staging of the shadow step (shadow_step_enqueue)
     bool stg_ready = false;
@@ -367,6 +379,19 @@ static void launch_ar_t(int n, dim3 grid, cudaStream_t s, const ArParams& P) {
     }
 }
 
+template <typename G>
+static void launch_os_t(int n, int grid, cudaStream_t s, const OsParams& P) {
+    switch (n) {
+        case 2: os_tap_kernel<G, 2><<<grid, kOsThreads, 0, s>>>(P); break;
+        case 3: os_tap_kernel<G, 3><<<grid, kOsThreads, 0, s>>>(P); break;
+        case 4: os_tap_kernel<G, 4><<<grid, kOsThreads, 0, s>>>(P); break;
+        case 5: os_tap_kernel<G, 5><<<grid, kOsThreads, 0, s>>>(P); break;
+        case 6: os_tap_kernel<G, 6><<<grid, kOsThreads, 0, s>>>(P); break;
+        case 7: os_tap_kernel<G, 7><<<grid, kOsThreads, 0, s>>>(P); break;
+        default: os_tap_kernel<G, 8><<<grid, kOsThreads, 0, s>>>(P); break;
+    }
+}
+
 static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaStream_t s) {
     if (P.rec_kind == kOptSgd) {
         // SGD-momentum: the warp-tiled data path only
@@ -509,6 +534,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "shadow_blocks" && value >= 1 && value <= 65535) c->shadow_blocks = (int)value;
     else if (k == "tma_blocks" && value >= 1 && value <= 65535) c->tma_blocks = (int)value;
     else if (k == "ar_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_max = (int)value;
+    else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else return fail(c, CM_ERR_ARG, "unknown parameter %s=%lld", key, (long long)value);
     return CM_OK;
 }
@@ -585,6 +611,9 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
     if (c->zero1 && (c->ce_tap || !c->staged_tap))
         return fail(c, CM_ERR_CONFIG, "CM_FLAG_ZERO1 needs the staged tap (no TAP_DIRECT / TAP_COPYENGINE)");
     c->shadow_place = cfg->shadow_place;
+    // one-shot push kernel for buckets <= 2 MiB / n (measured crossover vs two-shot: 1 MiB
+    // at n=2, 512 KiB at n=4; profiles/r01c_oneshot_sweep.md)
+    c->oneshot_max = std::min<int64_t>(kOsSlotBytes, (2ll << 20) / c->n);
     c->K = cfg->persist_every <= 1 ? 1 : cfg->persist_every;
     if (c->shadow_place == CM_SHADOW_DEVICE) c->K = 1;
     *out = c;   // returned even on failure so cm_last_error works; caller finalizes
@@ -682,12 +711,15 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
     b.dtype = c->dtype;
     b.layout_hash = c->layout_hash;
     b.padded_numel = c->P_pad;
-    void* ptrs[5] = {grad, p, m, v, c->pad};
+    // one-shot inbox (peer-mapped like the signal pad; a token allocation when n == 1)
+    const size_t inbox_bytes = c->n > 1 ? 2 * (size_t)c->n * kOsSlotBytes : 256;
+    CU(cudaMalloc(&c->inbox, inbox_bytes));
+    void* ptrs[6] = {grad, p, m, v, c->pad, c->inbox};
     PFN_getAddressRange getRange = nullptr;
     cudaDriverEntryPointQueryResult q;
     CU(cudaGetDriverEntryPoint("cuMemGetAddressRange", (void**)&getRange, cudaEnableDefault, &q));
     if (!getRange) return fail(c, CM_ERR_CUDA, "cuMemGetAddressRange unavailable");
-    for (int k = 0; k < 5; ++k) {
+    for (int k = 0; k < 6; ++k) {
         CUdeviceptr base = 0;
         size_t sz = 0;
         if (getRange(&base, &sz, (CUdeviceptr)ptrs[k]) != CUDA_SUCCESS)
@@ -740,9 +772,9 @@ cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
     // needed (B200_PROFILING.md: never spin across launches on one GPU).
     c->barriers = !(all_local && same_dev);
     for (int k = 0; k < c->n; ++k) {
-        void* ptr[5];
+        void* ptr[6];
         if (k == c->rank) {
-            for (int j = 0; j < 5; ++j) ptr[j] = (void*)B[k].raw[j];
+            for (int j = 0; j < 6; ++j) ptr[j] = (void*)B[k].raw[j];
         } else if (B[k].token == process_token()) {
             if (B[k].device != c->dev) {
                 cudaError_t e = cudaDeviceEnablePeerAccess(B[k].device, 0);
@@ -751,9 +783,9 @@ cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
                                 cudaGetErrorString(e));
                 cudaGetLastError();
             }
-            for (int j = 0; j < 5; ++j) ptr[j] = (void*)B[k].raw[j];
+            for (int j = 0; j < 6; ++j) ptr[j] = (void*)B[k].raw[j];
         } else {
-            for (int j = 0; j < 5; ++j) {
+            for (int j = 0; j < 6; ++j) {
                 cm_status s = open_peer(c, B[k], j, &ptr[j]);
                 if (s != CM_OK) return s;
             }
@@ -763,6 +795,7 @@ cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
         c->peer_m[k] = (float*)ptr[2];
         c->peer_v[k] = (float*)ptr[3];
         c->pads.p[k] = (uint32_t*)ptr[4];
+        c->peer_inbox[k] = (char*)ptr[5];
     }
     if (!c->no_tap) {
         cm_status s = create_or_attach_segment(c);
@@ -887,6 +920,24 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
     return CM_OK;
 }
 
+// Issue the pending tap drain: one copy-engine D2H of the run's contiguous source range into
+// the ring, then one launch that publishes the run's tap flags.  Small shards (Llama's
+// norm buckets, the one-shot path) would otherwise cost 4 API calls each on the host.
+static cm_status flush_drain(cm_ctx* c, cudaStream_t s) {
+    if (c->dr_b0 < 0) return CM_OK;
+    CU(cudaEventRecord(c->ev_ar, s));
+    CU(cudaStreamWaitEvent(c->cs_tap, c->ev_ar, 0));
+    CU(cudaMemcpyAsync(c->dr_dst, c->dr_src, c->dr_bytes, cudaMemcpyDeviceToHost, c->cs_tap));
+    const int slot = (int)(c->dr_iter % c->D);
+    volatile uint64_t* fl = to_dev(c, slot_flags(c, slot) + c->dr_b0);
+    publish_range_kernel<<<1, 32, 0, c->cs_tap>>>(fl, c->dr_b1 - c->dr_b0 + 1, (uint64_t)(c->dr_iter + 1));
+    c->launches++;
+    CHECK_LAUNCH();
+    c->dr_b0 = c->dr_b1 = -1;
+    c->dr_bytes = 0;
+    return CM_OK;
+}
+
 cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* stream) {
     if (!c) return CM_ERR_ARG;
     if (c->cuda_dead) return CM_ERR_CUDA;
@@ -971,7 +1022,41 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         P.tap_flag = to_dev(c, slot_flags(c, slot) + bucket);
         P.tap_flag_value = (uint64_t)(t + 1);
     }
-    if (!skip_kernel) {
+    // small buckets take the one-shot push kernel (multi-process ranks only:
+    // virtual ranks share one stream, where a rank cannot wait for its peers' pushes;
+    // they use the two-shot kernel, which computes the same rank-order sum)
+    const bool oneshot = c->n > 1 && c->barriers && !c->zero1 && B.padded * c->es <= c->oneshot_max;
+    if (oneshot && !skip_kernel) {
+        OsParams O{};
+        const int64_t bucket_bytes = B.padded * c->es;
+        const int h = (int)(P.epoch & 1);
+        O.own = c->peer_grad[c->rank] + B.off * c->es;
+        for (int k = 0; k < c->n; ++k) {
+            O.push[k] = c->peer_inbox[k] + ((size_t)h * c->n + c->rank) * kOsSlotBytes;
+            O.inbox[k] = c->inbox + ((size_t)h * c->n + k) * kOsSlotBytes;
+        }
+        O.tap = P.tap;
+        O.nvec = bucket_bytes / 16;
+        O.shard_lo = (int64_t)c->rank * (shard * c->es / 16);
+        O.shard_hi = O.shard_lo + shard * c->es / 16;
+        O.pads = c->pads;
+        O.epoch = P.epoch;
+        O.rank = c->rank;
+        const int og = (int)std::max<int64_t>(1, std::min<int64_t>((O.nvec + kOsThreads - 1) / kOsThreads,
+                                                                   kMaxBarrierBlocks));
+        if (fused_tap) {
+            O.done_ctr = c->d_done_ctr;
+            c->done_total += (unsigned long long)og - (unsigned long long)grid;   // grid was counted above
+            O.done_target = c->done_total;
+            O.tap_flag = P.tap_flag;
+            O.tap_flag_value = P.tap_flag_value;
+        }
+        TimedScope ts(c, 0, s);
+        if (c->dtype == CM_F32) launch_os_t<F32Tag>(c->n, og, s, O);
+        else launch_os_t<BF16Tag>(c->n, og, s, O);
+        c->launches++;
+        CHECK_LAUNCH();
+    } else if (!skip_kernel) {
         TimedScope ts(c, 0, s);
         if (c->dtype == CM_F32) launch_ar_t<F32Tag>(c->n, grid, s, P);
         else launch_ar_t<BF16Tag>(c->n, grid, s, P);
@@ -986,17 +1071,38 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         // half the kernel wrote, so the grad buffer is free as soon as the kernel is done.
         if (!c->cs_tap) CU(cudaStreamCreateWithFlags(&c->cs_tap, cudaStreamNonBlocking));
         if (!c->ev_ar) CU(cudaEventCreateWithFlags(&c->ev_ar, cudaEventDisableTiming));
-        CU(cudaEventRecord(c->ev_ar, s));
-        CU(cudaStreamWaitEvent(c->cs_tap, c->ev_ar, 0));
         const char* src = staged ? (const char*)c->stage_buf[t & 1] + B.shard_off * c->es
                                  : c->peer_grad[c->rank] + byte_off;
-        CU(cudaMemcpyAsync(ring_slot_host(c, slot) + B.shard_off * c->es, src, shard * c->es,
-                           cudaMemcpyDeviceToHost, c->cs_tap));
-        cm_status st = publish(c, (volatile int64_t*)(slot_flags(c, slot) + bucket), t + 1, c->cs_tap);
-        if (st != CM_OK) return st;
+        char* dst = ring_slot_host(c, slot) + B.shard_off * c->es;
+        const size_t bytes = (size_t)shard * c->es;
+        // coalesce with the pending drain when this shard continues it (same iteration, next
+        // bucket, contiguous source and destination); the pending run was launched before
+        // this bucket's kernel, so the merged copy waits for both (stream order)
+        const bool extend = c->dr_b0 >= 0 && c->dr_iter == t && bucket == c->dr_b1 + 1 &&
+                            src == c->dr_src + c->dr_bytes && dst == c->dr_dst + c->dr_bytes &&
+                            c->dr_bytes + bytes <= (size_t)kDrainCoalesce;
+        if (!extend) {
+            cm_status st = flush_drain(c, s);
+            if (st != CM_OK) return st;
+            c->dr_b0 = bucket;
+            c->dr_iter = t;
+            c->dr_src = src;
+            c->dr_dst = dst;
+        }
+        c->dr_b1 = bucket;
+        c->dr_bytes += bytes;
+        // a large run goes now; the iteration's last bucket flushes below
+        if (c->dr_bytes >= (size_t)kDrainCoalesce) {
+            cm_status st = flush_drain(c, s);
+            if (st != CM_OK) return st;
+        }
     }
     c->issued[bucket] = 1;
     c->issued_count++;
+    if (c->issued_count == (int)c->buckets.size()) {
+        cm_status st = flush_drain(c, s);
+        if (st != CM_OK) return st;
+    }
     if (!c->no_tap && c->issued_count == (int)c->buckets.size()) {
         const bool via_ce = c->ce_tap || staged;
         CU(cudaEventRecord(c->ev_tap_done[slot], via_ce ? c->cs_tap : s));
@@ -1470,6 +1576,8 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     c->shadow_enq = I;
     c->released_upto = I;   // step I is persisted (HOST) / held in HBM (DEVICE)
     c->stage_iter[0] = c->stage_iter[1] = -1;   // staging halves hold nothing of the new run
+    c->dr_b0 = c->dr_b1 = -1;                   // a partial iteration's pending drain is void
+    c->dr_bytes = 0;
     c->stage_consumer[0] = c->stage_consumer[1] = false;
     for (int i = 0; i < c->D; ++i) c->slot_sc_step[i] = -1;
     *restored = I;
@@ -1663,6 +1771,7 @@ cm_status cm_finalize(cm_ctx* c) {
     if (c->state_dev_alloc) cudaFree(c->state_dev_alloc);
     if (c->d_buckets) cudaFree(c->d_buckets);
     if (c->pad) cudaFree(c->pad);
+    if (c->inbox) cudaFree(c->inbox);
     if (c->d_done_ctr) cudaFree(c->d_done_ctr);
     if (c->d_bad) cudaFree(c->d_bad);
     for (auto e : c->ev_tap_done) cudaEventDestroy(e);

@@ -25,7 +25,9 @@ def counts():
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("mode", ["parity_f32", "parity_bf16", "parity_zero1", "parity_sgd", "restore_soft"])
+@pytest.mark.parametrize("mode", ["parity_f32", "parity_bf16", "parity_zero1", "parity_sgd",
+                                  "parity_oneshot", "parity_oneshot_bf16", "parity_oneshot_direct",
+                                  "restore_soft"])
 def test_multiprocess(mode):
     for n in counts():
         name = f"cmmp{os.getpid()}_{mode}_{n}"

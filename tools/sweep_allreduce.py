@@ -32,6 +32,12 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--ar-blocks", type=int, default=0, help="grid cap override (0 = library default)")
+    ap.add_argument("--min-kib", type=int, default=0, help="start size in KiB (overrides --min-mib)")
+    ap.add_argument("--max-kib", type=int, default=0, help="end size in KiB (overrides --max-mib)")
+    ap.add_argument("--burst", type=int, default=1,
+                    help="launches per timed rep (back to back, as in a step); time = total / burst")
+    ap.add_argument("--oneshot-max", type=int, default=-1,
+                    help="one-shot push kernel for buckets <= this many bytes (-1 = library default, 0 = off)")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -40,9 +46,11 @@ def main():
     dtype = cm.CM_F32 if args.dtype == "f32" else cm.CM_BF16
     es = 4 if dtype == cm.CM_F32 else 2
     dev = torch.device("cuda", local)
-    mib = args.min_mib
-    while mib <= args.max_mib:
-        S = mib << 20
+    kib = args.min_kib or args.min_mib * 1024
+    kib_max = args.max_kib or args.max_mib * 1024
+    while kib <= kib_max:
+        S = kib << 10
+        mib = kib
         numel = [S // es]
         stream = torch.cuda.Stream(dev, priority=-1)
         if args.mode == "nccl":
@@ -56,28 +64,33 @@ def main():
             R = harness.DistRank(numel, dtype, S + 1, name, 2, cm.CM_SHADOW_HOST, flags)
             if args.ar_blocks:
                 R.r.ctx.set_param("ar_blocks", args.ar_blocks)
+            if args.oneshot_max >= 0:
+                R.r.ctx.set_param("oneshot_max_bytes", args.oneshot_max)
             R.r.ctx.gen_grads(0, 0, 10, R.stream)
             R.stream.synchronize()
             stream = R.stream
             ctx = R.r.ctx
             fn = lambda t: ctx.allreduce_multicast(0, t, stream)   # noqa: E731
         times = []
+        it = 0
         with torch.cuda.stream(stream):
             for t in range(args.warmup + args.reps):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                fn(t)
+                for _ in range(args.burst):
+                    fn(it)
+                    it += 1
                 b.record(stream)
                 b.synchronize()
                 if t >= args.warmup:
-                    times.append(a.elapsed_time(b))
+                    times.append(a.elapsed_time(b) / args.burst)
         med = statistics.median(times)
         tt = torch.tensor([med], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         med = tt.item()
         if rank == 0:
             sec = med * 1e-3
-            print(json.dumps({"mode": args.mode, "ar_blocks": args.ar_blocks, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
+            print(json.dumps({"mode": args.mode, "burst": args.burst, "ar_blocks": args.ar_blocks, "oneshot_max": args.oneshot_max, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
                               "dtype": args.dtype, "n": n, "bytes": S, "ms": med,
                               "p10_ms": sorted(times)[len(times) // 10], "p90_ms": sorted(times)[9 * len(times) // 10],
                               "algbw_GBps": S / sec / 1e9, "busbw_GBps": 2 * (n - 1) / n * S / sec / 1e9,
@@ -88,7 +101,7 @@ def main():
             ctx.finalize()
             cm.unlink_shadow(name, rank)
         dist.barrier()
-        mib *= 2
+        kib *= 2
     dist.destroy_process_group()
 
 
