@@ -86,6 +86,15 @@ typedef enum { CM_SHADOW_HOST = 0, CM_SHADOW_DEVICE = 1 } cm_shadow_place;
                                          passed to cm_register_buckets are then shard-local
                                          arrays of P_pad/n elements.  Bit-identical to the
                                          unsharded path (same element arithmetic).         */
+#define CM_FLAG_NVLS (1ull << 6)       /* small buckets (the one-shot push kernel, SURVEY 8 row
+                                         f2, "PRE" multicast analog): each
+                                         rank pushes its bucket ONCE with multimem.st into an
+                                         NVLink-SHARP multicast inbox and the NVSwitch
+                                         replicates it to all n ranks (egress S_b instead of
+                                         (n-1) S_b).  cm_connect creates the multicast object
+                                         (rank 0) and hands it to the peers over a local Unix
+                                         socket; CM_ERR_CONFIG if the box has no multicast
+                                         support.  Multi-process ranks only.  Same bits.    */
 #define CM_FLAG_NO_SHADOW (1ull << 3) /* benchmark mode (bucket sweep): tap into the ring but
                                          keep no shadow replica and no flow control; the ring
                                          is overwritten freely; shadow/verify/restore refuse */

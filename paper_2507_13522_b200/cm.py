@@ -22,6 +22,7 @@ CM_FLAG_TAP_COPYENGINE = 1 << 2
 CM_FLAG_NO_SHADOW = 1 << 3
 CM_FLAG_ZERO1 = 1 << 5          # sharded AdamW state + fused parameter all-gather
 CM_FLAG_TAP_DIRECT = 1 << 4     # default tap is "staged" (HBM staging + copy-engine drain)
+CM_FLAG_NVLS = 1 << 6           # one-shot push through an NVLink-SHARP multicast inbox
 
 # every symbol include/cm.h declares (tests check the library exports all of them)
 EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",

@@ -36,6 +36,13 @@ __device__ __forceinline__ void st_cs_v4(void* p, const uint4& v) {
     asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};"
                  :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
+// NVLink-SHARP multicast store: one 16-byte store through a multicast address, replicated
+// by the NVSwitch into every bound device's memory (bits moved as-is, no arithmetic)
+__device__ __forceinline__ void mc_st_v4(void* p, const uint4& v) {
+    asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
+                    "f"(__uint_as_float(v.w)) : "memory");
+}
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
@@ -312,6 +319,7 @@ struct OsParams {
     char* push[kMaxRanks];         // peer k's inbox slot [rank] (unused for k == rank)
     const char* inbox[kMaxRanks];  // this rank's inbox slot [k] (unused for k == rank)
     char* tap;                     // tap target of this rank's shard (nullptr: no tap)
+    char* mc;                      // NVLS: multicast address of slot [rank] (nullptr: unicast)
     int64_t nvec;                  // 16-byte vectors in the bucket
     int64_t shard_lo, shard_hi;    // this rank's shard, in vectors
     Pads pads;
@@ -329,11 +337,16 @@ template <typename G, int N>
 __global__ void __launch_bounds__(kOsThreads) os_tap_kernel(const OsParams P) {
     const int64_t stride = (int64_t)gridDim.x * kOsThreads;
     const int64_t q0 = blockIdx.x * (int64_t)kOsThreads + threadIdx.x;
-    for (int64_t q = q0; q < P.nvec; q += stride) {          // push
-        const uint4 x = ld_v4(P.own + q * 16);
+    if (P.mc) {                                              // push once: the switch replicates
+        for (int64_t q = q0; q < P.nvec; q += stride) mc_st_v4(P.mc + q * 16, ld_v4(P.own + q * 16));
+        __threadfence_system();
+    } else {                                                 // push n-1 unicast copies
+        for (int64_t q = q0; q < P.nvec; q += stride) {
+            const uint4 x = ld_v4(P.own + q * 16);
 #pragma unroll
-        for (int k = 0; k < N; ++k)
-            if (k != P.rank) st_v4(P.push[k] + q * 16, x);
+            for (int k = 0; k < N; ++k)
+                if (k != P.rank) st_v4(P.push[k] + q * 16, x);
+        }
     }
     block_barrier(P.pads, N, P.rank, P.epoch, 0);            // every rank's chunk arrived
     for (int64_t q = q0; q < P.nvec; q += stride) {          // reduce from the local inbox

@@ -12,7 +12,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <poll.h>
 #include <sys/mman.h>
+#include <sys/socket.h>
+#include <sys/un.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -153,6 +156,12 @@ struct cm_ctx {
     uint32_t* pad = nullptr;
     char* inbox = nullptr;                // one-shot inbox: 2 halves x n slots x kOsSlotBytes
     char* peer_inbox[kMaxRanks] = {};
+    // NVLS (CM_FLAG_NVLS): the inbox is physical memory bound to a multicast object; pushes
+    // go through the multicast mapping mc_va, reads through the unicast mapping uc_va
+    bool nvls = false;
+    CUmemGenericAllocationHandle mc_handle = 0, mc_phys = 0;
+    CUdeviceptr mc_va = 0, uc_va = 0;
+    size_t mc_size = 0;
     int64_t oneshot_max = 0;              // buckets <= this many bytes use the one-shot kernel
     char* peer_grad[kMaxRanks] = {};
     float* peer_p[kMaxRanks] = {};
@@ -748,6 +757,213 @@ static cm_status open_peer(cm_ctx* c, const Blob& b, int k, void** out) {
 
 static cm_status create_or_attach_segment(cm_ctx* c);
 
+// ---------------------------------------------------------------- NVLS multicast inbox
+// SURVEY 8 row f2.  Rank 0 creates a multicast object (CUDA VMM), exports it as a POSIX
+// file descriptor and passes it to the peers over an abstract Unix socket (SCM_RIGHTS);
+// every rank adds its device, binds its own physical inbox, and maps both the multicast
+// address (pushes) and its own unicast address (reads).  The socket carries three
+// rendezvous points: all devices added -> bind; all bound -> use.
+namespace {
+struct Drv {
+    CUresult (*mcCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*);
+    CUresult (*mcAddDevice)(CUmemGenericAllocationHandle, CUdevice);
+    CUresult (*mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                          unsigned long long);
+    CUresult (*mcGran)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags);
+    CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+    CUresult (*memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+    CUresult (*memRelease)(CUmemGenericAllocationHandle);
+    CUresult (*memExport)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long);
+    CUresult (*memImport)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
+    CUresult (*addrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+    CUresult (*addrFree)(CUdeviceptr, size_t);
+    CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+    CUresult (*memUnmap)(CUdeviceptr, size_t);
+    CUresult (*setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+    CUresult (*devAttr)(int*, CUdevice_attribute, CUdevice);
+    bool ok = false;
+};
+Drv& drv() {
+    static Drv d = [] {
+        Drv x{};
+        cudaDriverEntryPointQueryResult q;
+        bool ok = true;
+        auto get = [&](const char* name, void** fn) {
+            if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess || !*fn) ok = false;
+        };
+        get("cuMulticastCreate", (void**)&x.mcCreate);
+        get("cuMulticastAddDevice", (void**)&x.mcAddDevice);
+        get("cuMulticastBindMem", (void**)&x.mcBindMem);
+        get("cuMulticastGetGranularity", (void**)&x.mcGran);
+        get("cuMulticastUnbind", (void**)&x.mcUnbind);
+        get("cuMemCreate", (void**)&x.memCreate);
+        get("cuMemRelease", (void**)&x.memRelease);
+        get("cuMemExportToShareableHandle", (void**)&x.memExport);
+        get("cuMemImportFromShareableHandle", (void**)&x.memImport);
+        get("cuMemAddressReserve", (void**)&x.addrReserve);
+        get("cuMemAddressFree", (void**)&x.addrFree);
+        get("cuMemMap", (void**)&x.memMap);
+        get("cuMemUnmap", (void**)&x.memUnmap);
+        get("cuMemSetAccess", (void**)&x.setAccess);
+        get("cuDeviceGetAttribute", (void**)&x.devAttr);
+        x.ok = ok;
+        return x;
+    }();
+    return d;
+}
+
+bool sock_send(int fd, const void* p, size_t n, int pass_fd = -1) {
+    struct iovec io = {(void*)p, n};
+    struct msghdr m = {};
+    m.msg_iov = &io;
+    m.msg_iovlen = 1;
+    char cbuf[CMSG_SPACE(sizeof(int))] = {};
+    if (pass_fd >= 0) {
+        m.msg_control = cbuf;
+        m.msg_controllen = sizeof cbuf;
+        struct cmsghdr* h = CMSG_FIRSTHDR(&m);
+        h->cmsg_level = SOL_SOCKET;
+        h->cmsg_type = SCM_RIGHTS;
+        h->cmsg_len = CMSG_LEN(sizeof(int));
+        memcpy(CMSG_DATA(h), &pass_fd, sizeof(int));
+    }
+    return sendmsg(fd, &m, MSG_NOSIGNAL) == (ssize_t)n;
+}
+
+bool sock_recv(int fd, void* p, size_t n, int* got_fd = nullptr, int timeout_ms = 120000) {
+    struct pollfd pf = {fd, POLLIN, 0};
+    if (poll(&pf, 1, timeout_ms) != 1) return false;
+    struct iovec io = {p, n};
+    struct msghdr m = {};
+    m.msg_iov = &io;
+    m.msg_iovlen = 1;
+    char cbuf[CMSG_SPACE(sizeof(int))] = {};
+    m.msg_control = cbuf;
+    m.msg_controllen = sizeof cbuf;
+    if (recvmsg(fd, &m, MSG_WAITALL) != (ssize_t)n) return false;
+    if (got_fd) {
+        *got_fd = -1;
+        for (struct cmsghdr* h = CMSG_FIRSTHDR(&m); h; h = CMSG_NXTHDR(&m, h))
+            if (h->cmsg_level == SOL_SOCKET && h->cmsg_type == SCM_RIGHTS) memcpy(got_fd, CMSG_DATA(h), sizeof(int));
+    }
+    return true;
+}
+}  // namespace
+
+#define DRV(call)                                                                               \
+    do {                                                                                        \
+        CUresult r_ = (call);                                                                   \
+        if (r_ != CUDA_SUCCESS) { err = #call; code = (int)r_; goto out; }                     \
+    } while (0)
+
+static cm_status setup_nvls(cm_ctx* c, uint64_t job_token) {
+    Drv& d = drv();
+    if (!d.ok) return fail(c, CM_ERR_CONFIG, "CM_FLAG_NVLS: driver multicast entry points unavailable");
+    int mc_ok = 0;
+    d.devAttr(&mc_ok, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, c->dev);
+    if (!mc_ok) return fail(c, CM_ERR_CONFIG, "CM_FLAG_NVLS: device %d has no NVLink multicast", c->dev);
+    const char* err = nullptr;
+    int code = 0;
+    int lfd = -1, fds[kMaxRanks] = {-1, -1, -1, -1, -1, -1, -1, -1}, mcfd = -1;
+    char tok = 0;
+    CUmulticastObjectProp mp = {};
+    size_t gran = 0;
+    struct sockaddr_un addr = {};
+    addr.sun_family = AF_UNIX;
+    // abstract name, unique per job (rank 0's process token) and layout
+    const int nl = snprintf(addr.sun_path + 1, sizeof(addr.sun_path) - 1, "cmnvls.%016llx.%016llx",
+                            (unsigned long long)job_token, (unsigned long long)c->layout_hash);
+    const socklen_t alen = (socklen_t)(offsetof(struct sockaddr_un, sun_path) + 1 + nl);
+    mp.numDevices = (unsigned)c->n;
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = 2 * (size_t)c->n * kOsSlotBytes;
+    DRV(d.mcGran(&gran, &mp, CU_MULTICAST_GRANULARITY_MINIMUM));
+    c->mc_size = (mp.size + gran - 1) / gran * gran;
+    mp.size = c->mc_size;
+    if (c->rank == 0) {
+        lfd = socket(AF_UNIX, SOCK_STREAM, 0);
+        if (lfd < 0 || bind(lfd, (struct sockaddr*)&addr, alen) != 0 || listen(lfd, kMaxRanks) != 0) {
+            err = "socket/bind/listen";
+            goto out;
+        }
+        DRV(d.mcCreate(&c->mc_handle, &mp));
+        DRV(d.memExport(&mcfd, c->mc_handle, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+        for (int k = 1; k < c->n; ++k) {
+            struct pollfd pf = {lfd, POLLIN, 0};
+            if (poll(&pf, 1, 120000) != 1) { err = "accept timeout"; goto out; }
+            int a = accept(lfd, nullptr, nullptr);
+            int32_t who = -1;
+            if (a < 0 || !sock_recv(a, &who, sizeof who) || who < 1 || who >= c->n || fds[who] >= 0) {
+                if (a >= 0) close(a);
+                err = "bad peer";
+                goto out;
+            }
+            fds[who] = a;
+            if (!sock_send(a, &c->mc_size, sizeof c->mc_size, mcfd)) { err = "send fd"; goto out; }
+        }
+    } else {
+        fds[0] = socket(AF_UNIX, SOCK_STREAM, 0);
+        int tries = 0;
+        while (connect(fds[0], (struct sockaddr*)&addr, alen) != 0) {
+            if (++tries > 12000) { err = "connect to rank 0"; goto out; }
+            usleep(10000);
+        }
+        int32_t me = c->rank;
+        size_t sz = 0;
+        if (!sock_send(fds[0], &me, sizeof me) || !sock_recv(fds[0], &sz, sizeof sz, &mcfd) || mcfd < 0 ||
+            sz != c->mc_size) {
+            err = "receive multicast handle";
+            goto out;
+        }
+        DRV(d.memImport(&c->mc_handle, (void*)(uintptr_t)mcfd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+    }
+    DRV(d.mcAddDevice(c->mc_handle, (CUdevice)c->dev));
+    // rendezvous 1: every device added before anyone binds memory; 2: every inbox bound
+    for (int phase = 0; phase < 2; ++phase) {
+        if (phase == 1) {
+            CUmemAllocationProp ap = {};
+            ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+            ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+            ap.location.id = c->dev;
+            ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;   // as the multicast object
+            DRV(d.memCreate(&c->mc_phys, c->mc_size, &ap, 0));
+            DRV(d.mcBindMem(c->mc_handle, 0, c->mc_phys, 0, c->mc_size, 0));
+        }
+        if (c->rank == 0) {
+            for (int k = 1; k < c->n; ++k)
+                if (!sock_recv(fds[k], &tok, 1)) { err = "rendezvous (peer)"; goto out; }
+            for (int k = 1; k < c->n; ++k)
+                if (!sock_send(fds[k], &tok, 1)) { err = "rendezvous (root)"; goto out; }
+        } else if (!sock_send(fds[0], &tok, 1) || !sock_recv(fds[0], &tok, 1)) {
+            err = "rendezvous";
+            goto out;
+        }
+    }
+    {
+        CUmemAccessDesc ad = {};
+        ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        ad.location.id = c->dev;
+        ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        DRV(d.addrReserve(&c->mc_va, c->mc_size, gran, 0, 0));
+        DRV(d.memMap(c->mc_va, c->mc_size, 0, c->mc_handle, 0));
+        DRV(d.setAccess(c->mc_va, c->mc_size, &ad, 1));
+        DRV(d.addrReserve(&c->uc_va, c->mc_size, gran, 0, 0));
+        DRV(d.memMap(c->uc_va, c->mc_size, 0, c->mc_phys, 0));
+        DRV(d.setAccess(c->uc_va, c->mc_size, &ad, 1));
+    }
+    c->nvls = true;
+out:
+    if (mcfd >= 0) close(mcfd);
+    if (lfd >= 0) close(lfd);
+    for (int k = 0; k < kMaxRanks; ++k)
+        if (fds[k] >= 0) close(fds[k]);
+    if (!c->nvls)
+        return fail(c, CM_ERR_CONFIG, "CM_FLAG_NVLS setup failed at %s (CUresult %d, errno %d)", err ? err : "?",
+                    code, errno);
+    return CM_OK;
+}
+#undef DRV
+
 cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
     if (!c) return CM_ERR_ARG;
     if (c->cuda_dead) return CM_ERR_CUDA;
@@ -796,6 +1012,11 @@ cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
         c->peer_v[k] = (float*)ptr[3];
         c->pads.p[k] = (uint32_t*)ptr[4];
         c->peer_inbox[k] = (char*)ptr[5];
+    }
+    if ((c->cfg.flags & CM_FLAG_NVLS) && c->n > 1) {
+        if (!c->barriers) return fail(c, CM_ERR_CONFIG, "CM_FLAG_NVLS needs one process per GPU");
+        cm_status s = setup_nvls(c, B[0].token);
+        if (s != CM_OK) return s;
     }
     if (!c->no_tap) {
         cm_status s = create_or_attach_segment(c);
@@ -1033,8 +1254,10 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         O.own = c->peer_grad[c->rank] + B.off * c->es;
         for (int k = 0; k < c->n; ++k) {
             O.push[k] = c->peer_inbox[k] + ((size_t)h * c->n + c->rank) * kOsSlotBytes;
-            O.inbox[k] = c->inbox + ((size_t)h * c->n + k) * kOsSlotBytes;
+            const char* in = c->nvls ? (const char*)c->uc_va : c->inbox;
+            O.inbox[k] = in + ((size_t)h * c->n + k) * kOsSlotBytes;
         }
+        if (c->nvls) O.mc = (char*)c->mc_va + ((size_t)h * c->n + c->rank) * kOsSlotBytes;
         O.tap = P.tap;
         O.nvec = bucket_bytes / 16;
         O.shard_lo = (int64_t)c->rank * (shard * c->es / 16);
@@ -1772,6 +1995,16 @@ cm_status cm_finalize(cm_ctx* c) {
     if (c->d_buckets) cudaFree(c->d_buckets);
     if (c->pad) cudaFree(c->pad);
     if (c->inbox) cudaFree(c->inbox);
+    if (c->nvls) {
+        Drv& d = drv();
+        d.memUnmap(c->mc_va, c->mc_size);
+        d.addrFree(c->mc_va, c->mc_size);
+        d.memUnmap(c->uc_va, c->mc_size);
+        d.addrFree(c->uc_va, c->mc_size);
+        d.mcUnbind(c->mc_handle, (CUdevice)c->dev, 0, c->mc_size);
+        d.memRelease(c->mc_phys);
+        d.memRelease(c->mc_handle);
+    }
     if (c->d_done_ctr) cudaFree(c->d_done_ctr);
     if (c->d_bad) cudaFree(c->d_bad);
     for (auto e : c->ev_tap_done) cudaEventDestroy(e);

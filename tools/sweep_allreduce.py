@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--ar-blocks", type=int, default=0, help="grid cap override (0 = library default)")
     ap.add_argument("--min-kib", type=int, default=0, help="start size in KiB (overrides --min-mib)")
     ap.add_argument("--max-kib", type=int, default=0, help="end size in KiB (overrides --max-mib)")
+    ap.add_argument("--nvls", action="store_true", help="CM_FLAG_NVLS: one-shot push via multimem.st")
     ap.add_argument("--burst", type=int, default=1,
                     help="launches per timed rep (back to back, as in a step); time = total / burst")
     ap.add_argument("--oneshot-max", type=int, default=-1,
@@ -61,6 +62,8 @@ def main():
             flags = {"ours_tap": cm.CM_FLAG_NO_SHADOW, "ours": cm.CM_FLAG_NO_TAP,
                      "ours_tap_direct": cm.CM_FLAG_NO_SHADOW | cm.CM_FLAG_TAP_DIRECT}[args.mode]
             name = f"cmsw_{os.environ.get('MASTER_PORT', '0')}_{mib}"
+            if args.nvls:
+                flags |= cm.CM_FLAG_NVLS
             R = harness.DistRank(numel, dtype, S + 1, name, 2, cm.CM_SHADOW_HOST, flags)
             if args.ar_blocks:
                 R.r.ctx.set_param("ar_blocks", args.ar_blocks)
@@ -90,7 +93,7 @@ def main():
         med = tt.item()
         if rank == 0:
             sec = med * 1e-3
-            print(json.dumps({"mode": args.mode, "burst": args.burst, "ar_blocks": args.ar_blocks, "oneshot_max": args.oneshot_max, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
+            print(json.dumps({"mode": args.mode + ("_nvls" if args.nvls else ""), "burst": args.burst, "ar_blocks": args.ar_blocks, "oneshot_max": args.oneshot_max, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
                               "dtype": args.dtype, "n": n, "bytes": S, "ms": med,
                               "p10_ms": sorted(times)[len(times) // 10], "p90_ms": sorted(times)[9 * len(times) // 10],
                               "algbw_GBps": S / sec / 1e9, "busbw_GBps": 2 * (n - 1) / n * S / sec / 1e9,
