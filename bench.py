@@ -436,10 +436,29 @@ def run_ours_nockpt(args, rank, world, local, numel, dtype, cap):
     R.sync()
     dist.barrier()
     torch.cuda.synchronize()
+    R.r.ctx.timing(True)
     ms = time_steps(R.step, [R.stream], args.steps)
+    kms, kcnt = R.r.ctx.timing(False)
     ms = max_over_ranks(ms)
+    out = {"ms_step": ms / args.steps, "iters_per_s": 1000.0 / (ms / args.steps)}
+    n = dist.get_world_size()
+    if kcnt[0] and n > 1:
+        # the all-reduce kernel in lockstep (no host-link traffic skewing the ranks): its own
+        # NVLink roofline.  busBW bytes per launch = 2(n-1)/n * average bucket bytes.
+        info = R.r.ctx.info()
+        es = 4 if dtype == cm.CM_F32 else 2
+        Sb = info.padded_numel * es / info.n_buckets
+        ar_ms = max_over_ranks(kms[0] / kcnt[0])
+        nvl = 2 * (n - 1) / n * Sb * (0.5 if args.zero1 else 1.0)
+        out["rs_tap_ag"] = {"avg_ms": ar_ms, "launches": kcnt[0], "bound": "nvlink", "unit": "GB/s",
+                            "achieved": nvl / (ar_ms * 1e-3) / 1e9, "peak": NVLINK_PEAK_GBS,
+                            "frac": nvl / (ar_ms * 1e-3) / 1e9 / NVLINK_PEAK_GBS, "bytes_per_launch": nvl,
+                            "what": "all-reduce kernel without tap, ranks in lockstep (average bucket)"}
+    if kcnt[1]:
+        ad_ms = max_over_ranks(kms[1] / kcnt[1])
+        out["adamw_ms"] = ad_ms
     R.r.ctx.finalize()
-    return {"ms_step": ms / args.steps, "iters_per_s": 1000.0 / (ms / args.steps)}
+    return out
 
 
 # ---------------------------------------------------------------------------- oracle arm
