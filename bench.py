@@ -152,8 +152,14 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------- measurements
 def host_link_peaks(dev):
-    """Copy-engine pinned D2H / H2D GB/s on this GPU (the practical host-link roof)."""
+    """Copy-engine pinned D2H / H2D GB/s on this GPU (the practical host-link roof).  All
+    ranks measure at the same time (barrier first): with N GPUs writing host memory at
+    once the per-GPU share is what the checkpointed step can use."""
     import torch
+    import torch.distributed as dist
+    if dist.is_initialized():
+        dist.barrier()
+        torch.cuda.synchronize()
     n = 256 << 20
     d = torch.empty(n, dtype=torch.uint8, device=dev)
     h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
@@ -264,7 +270,10 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     ar_hbm = 2 * Sb + (Sb / n if args.tap == "staged" else 0)    # local + peers' reads/writes (+ staging)
     if n == 1:
         ar_hbm = (2 * Sb) if args.tap == "staged" else Sb        # copy to staging / read for a direct tap
-    ent = {"avg_ms": ar_ms, "launches": kcnt[0], "share": kms[0] / ms}
+    ent = {"avg_ms": ar_ms, "launches": kcnt[0], "share": kms[0] / ms,
+           "note": "in-step launch time: includes the entry-barrier wait for the slowest rank (the "
+                   "checkpointed synthetic step is host-link bound and skews the ranks); the kernel's "
+                   "own roofline is nockpt_ours.rs_tap_ag (ranks in lockstep)" if n > 1 else ""}
     if n > 1:
         ent.update(bound="nvlink", achieved=ar_nvl / (ar_ms * 1e-3) / 1e9, peak=NVLINK_PEAK_GBS, unit="GB/s",
                    bytes_per_launch=ar_nvl, peak_source="B200_PROFILING.md measured peer copy, per direction")
@@ -313,16 +322,21 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     # the step's binding resource: the host link carries the tap (S/n per GPU) and the
     # persisted shadow state (12 L / K); our kernels each run near their own roofs
     step_d2h = S_bytes / n + sh_d2h
+    # lower bounds of one step per resource (algorithmic bytes / peak); the largest binds
     t_link = step_d2h / (link["d2h"] * 1e9)
-    t_kern = max(kms[0], kms[1]) / args.steps * 1e-3
+    lb = {"rs_tap_ag": nb * kern["rs_tap_ag"]["bytes_per_launch"] / (kern["rs_tap_ag"]["peak"] * 1e9),
+          "adamw_step": kern["adamw_step"]["bytes_per_launch"] / (kern["adamw_step"]["peak"] * 1e9)}
+    t_kern = max(lb.values())
     if t_link >= t_kern:
         roof = {"kernel": "tap drain + shadow persist (copy engines, host link D2H)", "bound": "host_link",
                 "achieved": step_d2h / (ms_step * 1e-3) / 1e9, "peak": link["d2h"], "unit": "GB/s",
                 "bytes_per_step": step_d2h, "peak_source": "measured pinned D2H copy (this run)",
                 "note": "the checkpointed step in synthetic mode (no compute to hide under) is bound by the "
-                        "host link; per-kernel rooflines are in 'kernels'"}
+                        "host link (lower bound %.2f ms vs %.2f ms for the largest kernel); peak = per-GPU "
+                        "D2H with all ranks copying at once; per-kernel rooflines are in 'kernels'"
+                        % (t_link * 1e3, t_kern * 1e3)}
     else:
-        dk = "rs_tap_ag" if kms[0] >= kms[1] else "adamw_step"
+        dk = max(lb, key=lb.get)
         roof = {"kernel": dk, **{k: kern[dk][k] for k in ("bound", "achieved", "peak", "unit", "bytes_per_launch",
                                                            "peak_source")}}
     roof["frac"] = roof["achieved"] / roof["peak"]
