@@ -248,6 +248,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
         ms = time_steps(step, [R.stream, R.side], args.steps, ctx)
     kms, kcnt = ctx.timing(False)
     launches = ctx.info().launches - launches0
+    drain_now = ctx.info().drain_ctas
     ms_max = max_over_ranks(ms)
     ms_step = ms_max / args.steps
     iters_per_s = 1000.0 / ms_step
@@ -344,7 +345,8 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
 
     result = {"ms_step": ms_step, "iters_per_s": iters_per_s, "launches": launches, "kernels": kern,
               "roofline": roof, "clocks": clk.summary(), "shadow_bit_identical": mismatch == -1,
-              "host_link_GBps": link, "S_bytes": S_bytes}
+              "host_link_GBps": link, "S_bytes": S_bytes,
+              "drain": "copy engine" if drain_now == 0 else f"SM drain, {drain_now} CTA(s)"}
 
     # ----- e2e: same metric through the public API with HOST gradient buffers
     if not args.no_e2e:
@@ -571,6 +573,7 @@ def main():
             "dtype": "f32" if dtype == cm.CM_F32 else "bf16-grads/f32-state", "data": "synthetic",
             "config": {"workload": name, "ranks": world, "shadow": args.shadow, "ring_depth": args.ring_depth,
                        "tap": args.tap, "persist_every": args.persist_every, "zero1": args.zero1,
+                       "drain": res["drain"] + " (library auto policy)",
                        "parallelism": f"dp{world}", "l2": "inputs larger than L2 (working set >> 126 MB)",
                        "iters_per_s": res["iters_per_s"]},
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res.get("e2e"),

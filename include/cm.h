@@ -284,7 +284,9 @@ cm_status cm_verify(cm_ctx *ctx, int64_t *mismatch, void *stream);
 /* Introspection (host-only, cheap). */
 typedef struct {
     int32_t n_buckets, world_size, rank, ring_depth, grad_dtype, shadow_place, peers_in_process;
-    int32_t reserved;
+    int32_t drain_ctas;                 /* how tap drains / snapshot persists reach the host
+                                           now: 0 copy engine, k > 0 a k-CTA SM drain kernel
+                                           (cm_set_param "drain_ctas": -1 auto, the default) */
     int64_t padded_numel, shard_numel;  /* P_pad; sum over buckets of E_b/n               */
     int64_t shadow_step;                /* last step the shadow published                 */
     int64_t launches;                   /* kernels this context launched so far           */

@@ -843,6 +843,19 @@ __global__ void __launch_bounds__(256) compare_kernel(const float* __restrict__ 
     }
 }
 
+// ------------------------------------------------------------------ low-intensity D2H drain
+// A copy engine drains at the host link's full rate, and a saturated device->host link
+// delays the GPU's own command fetch: measured, a launch-bound kernel stream runs 17%
+// slower next to a 32 GB/s copy-engine drain and not measurably slower next to an 11 GB/s
+// single-CTA SM drain (profiles/r01c_interference.md).  With compute to hide under, the
+// tap drain and the snapshot persist therefore go through this kernel: `gridDim.x` CTAs
+// (1 by default) copy 16-byte vectors from HBM into host-mapped memory with streaming
+// stores; the link never saturates, and a few SM slots are the only cost.
+__global__ void __launch_bounds__(256) drain_kernel(const uint4* __restrict__ src, uint4* dst, int64_t nvec) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nvec; q += (int64_t)gridDim.x * blockDim.x)
+        st_cs_v4(dst + q, ld_cs_v4(src + q));
+}
+
 // stream-ordered store of one int64 into host-mapped memory (segment header)
 __global__ void publish_kernel(volatile int64_t* dst, int64_t value) {
     __threadfence_system();

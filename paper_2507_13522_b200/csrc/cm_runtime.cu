@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -163,6 +164,11 @@ struct cm_ctx {
     CUdeviceptr mc_va = 0, uc_va = 0;
     size_t mc_size = 0;
     int64_t oneshot_max = 0;              // buckets <= this many bytes use the one-shot kernel
+    bool ablate_no_drain = false;         // ablation only: staged taps never reach the host ring
+    int drain_ctas = -1;                  // D2H of tap drains / persists: 0 copy engine, k>0 k-CTA SM
+                                          // drain, -1 auto (SM drain when the link demand is low)
+    double iter_period_s = 0.0;           // EMA of the host period between training steps
+    std::chrono::steady_clock::time_point last_step_time{};
     char* peer_grad[kMaxRanks] = {};
     float* peer_p[kMaxRanks] = {};
     float* peer_m[kMaxRanks] = {};
@@ -544,6 +550,10 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "tma_blocks" && value >= 1 && value <= 65535) c->tma_blocks = (int)value;
     else if (k == "ar_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_max = (int)value;
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
+    else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
+    // cost decomposition only (tools/model_mode.py): the staged tap's copy-engine drain is not
+    // issued, so the ring is never written -- restore and the host-ring fallback are invalid
+    else if (k == "ablate_no_drain" && (value == 0 || value == 1) && c->no_shadow) c->ablate_no_drain = value;
     else return fail(c, CM_ERR_ARG, "unknown parameter %s=%lld", key, (long long)value);
     return CM_OK;
 }
@@ -1141,6 +1151,37 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
     return CM_OK;
 }
 
+// Device -> host copy into the pinned, mapped segment on stream s: copy engine (full link
+// rate), or with drain_ctas > 0 the low-intensity SM drain kernel (host pointer -> its
+// device alias).  Both are stream-ordered like the other, so flags published after it on
+// the same stream follow the data (posted writes stay ordered).
+// Auto policy (drain_ctas = -1): the per-iteration D2H demand (tap S/n + snapshot 12 L / K)
+// over the measured step period.  Below kSmDrainRate the single-CTA SM drain (~11 GB/s) keeps
+// up at a third of its rate or less and the link stays far from saturation; above it the
+// step is link-bound and the copy engine's full rate matters more than interference.
+constexpr double kSmDrainRate = 4.5e9;
+static int drain_ctas_now(const cm_ctx* c) {
+    if (c->drain_ctas >= 0) return c->drain_ctas;
+    if (c->iter_period_s <= 0.0) return 0;
+    double bytes = (double)c->shard_numel * c->es;
+    if (c->shadow_place == CM_SHADOW_HOST && !c->no_shadow) bytes += 12.0 * (double)c->shard_numel / c->K;
+    return bytes / c->iter_period_s < kSmDrainRate ? 1 : 0;
+}
+
+static cm_status d2h(cm_ctx* c, char* host_dst, const void* dev_src, size_t bytes, cudaStream_t s) {
+    const int ctas = drain_ctas_now(c);
+    if (ctas <= 0 || (bytes & 15) || ((uintptr_t)dev_src & 15) || ((uintptr_t)host_dst & 15)) {
+        CU(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, s));
+        return CM_OK;
+    }
+    const int64_t nvec = (int64_t)(bytes / 16);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, (nvec + 255) / 256));
+    drain_kernel<<<grid, 256, 0, s>>>((const uint4*)dev_src, (uint4*)to_dev(c, host_dst), nvec);
+    c->launches++;
+    CHECK_LAUNCH();
+    return CM_OK;
+}
+
 // Issue the pending tap drain: one copy-engine D2H of the run's contiguous source range into
 // the ring, then one launch that publishes the run's tap flags.  Small shards (Llama's
 // norm buckets, the one-shot path) would otherwise cost 4 API calls each on the host.
@@ -1148,7 +1189,10 @@ static cm_status flush_drain(cm_ctx* c, cudaStream_t s) {
     if (c->dr_b0 < 0) return CM_OK;
     CU(cudaEventRecord(c->ev_ar, s));
     CU(cudaStreamWaitEvent(c->cs_tap, c->ev_ar, 0));
-    CU(cudaMemcpyAsync(c->dr_dst, c->dr_src, c->dr_bytes, cudaMemcpyDeviceToHost, c->cs_tap));
+    {
+        cm_status st = d2h(c, c->dr_dst, c->dr_src, c->dr_bytes, c->cs_tap);
+        if (st != CM_OK) return st;
+    }
     const int slot = (int)(c->dr_iter % c->D);
     volatile uint64_t* fl = to_dev(c, slot_flags(c, slot) + c->dr_b0);
     publish_range_kernel<<<1, 32, 0, c->cs_tap>>>(fl, c->dr_b1 - c->dr_b0 + 1, (uint64_t)(c->dr_iter + 1));
@@ -1286,7 +1330,7 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         c->launches++;
         CHECK_LAUNCH();
     }
-    if (!c->no_tap && (c->ce_tap || staged)) {
+    if (!c->no_tap && (c->ce_tap || staged) && !c->ablate_no_drain) {
         // copy-engine drain of the reduced shard to the host ring, decoupled from the training
         // stream: it overlaps the next buckets' all-reduce, the AdamW and (model mode) the
         // backward.  CE mode reads the grad buffer back (cm_apply_step then waits for these
@@ -1373,6 +1417,14 @@ cm_status cm_apply_step_sgd(cm_ctx* c, int64_t step, const cm_sgd* hp, void* str
 }
 
 static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* stream) {
+    {   // step period (host clock; the stream's backpressure ties it to the GPU's pace)
+        const auto now = std::chrono::steady_clock::now();
+        if (c->train_step > 0) {
+            const double dt = std::chrono::duration<double>(now - c->last_step_time).count();
+            c->iter_period_s = c->iter_period_s > 0.0 ? 0.8 * c->iter_period_s + 0.2 * dt : dt;
+        }
+        c->last_step_time = now;
+    }
     const int slot = (int)((step - 1) % c->D);
     c->slot_sc[slot] = rec;
     c->slot_sc_step[slot] = step;
@@ -1512,8 +1564,10 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
                 CU(cudaStreamWaitEvent(c->cs_d2h, c->ev_stg_free[j], 0));
                 // SGD leaves v untouched (all zero in every half): p and the velocity only
                 for (int k = 0; k < (rec.kind == kOptSgd ? 2 : 3); ++k)
-                    CU(cudaMemcpyAsync(c->sh[ph][k] + lo, c->sd[hout][k] + lo, (size_t)len * 4,
-                                       cudaMemcpyDeviceToHost, c->cs_d2h));
+                {
+                    cm_status pst = d2h(c, (char*)(c->sh[ph][k] + lo), c->sd[hout][k] + lo, (size_t)len * 4, c->cs_d2h);
+                    if (pst != CM_OK) return pst;
+                }
             }
         }
         CU(cudaEventRecord(c->ev_join, c->cs_k));
@@ -1818,6 +1872,7 @@ cm_status cm_get_info(const cm_ctx* c, cm_info* o) {
     o->grad_dtype = c->dtype;
     o->shadow_place = c->shadow_place;
     o->peers_in_process = c->in_process ? 1 : 0;
+    o->drain_ctas = drain_ctas_now(c);
     o->padded_numel = c->P_pad;
     o->shard_numel = c->shard_numel;
     o->shadow_step = c->hdr ? c->hdr->shadow_step : -1;

@@ -98,7 +98,7 @@ def run_arm(arm, args, rank, world, local):
         place = cm.CM_SHADOW_DEVICE if args.shadow == "device" else cm.CM_SHADOW_HOST
         D = 2 if arm == "ours_nockpt" else args.ring_depth
         R = harness.DistRank(numel, cm.CM_BF16, W.CAP_BYTES, name, D, place, flags,
-                             persist_every=args.persist_every)
+                             persist_every=1 if arm == "ours_nockpt" else args.persist_every)
         buckets = R.r.buckets()
         comm = torch.cuda.Stream(dev, priority=-1)
         ctx = R.r.ctx

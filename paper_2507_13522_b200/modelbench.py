@@ -42,23 +42,60 @@ def run_arm(arm, args, rank, world, local):
         streams = []
         cleanup = lambda: None   # noqa: E731
     else:
-        flags = cm.CM_FLAG_NO_TAP if arm == "ours_nockpt" else (
+        flags = cm.CM_FLAG_NO_TAP if arm in ("ours_nockpt", "nockpt_d2hload", "nockpt_d2hpaced") else (
             {"ce": cm.CM_FLAG_TAP_COPYENGINE, "direct": cm.CM_FLAG_TAP_DIRECT}.get(args.tap, 0))
-        if arm == "ours_tap_only":                  # tap into the ring, no shadow replica
+        if arm in ("ours_tap_only", "ours_tap_nodrain"):   # tap into the ring, no shadow replica
             flags |= cm.CM_FLAG_NO_SHADOW
         if getattr(args, "zero1", False):
             flags |= cm.CM_FLAG_ZERO1
         name = f"cmmm_{os.environ.get('MASTER_PORT', '0')}_{arm}"
         cd = CheckmateDDP(model, local, world, rank, shm_name=name, ring_depth=args.ring_depth,
                           persist_every=args.persist_every, flags=flags)
+        if getattr(args, "drain_ctas", -1) != -1:   # override the library's auto drain policy
+            cd.r.ctx.set_param("drain_ctas", args.drain_ctas)
+        if arm == "ours_tap_nodrain":               # cost decomposition: staging stores, no D2H
+            cd.r.ctx.set_param("ablate_no_drain", 1)
+        load = None
+        pace = None
+        if arm == "nockpt_d2hpaced":                # the same bytes, released in small chunks
+            nb = cd.r.padded * 4 // world           # from forward pre-hooks (one per module)
+            src = torch.empty(nb, dtype=torch.uint8, device=dev)
+            dst = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+            ls = torch.cuda.Stream(dev)
+            mods = [m for m in model.modules() if len(list(m.children())) == 0]
+            cs = (nb + len(mods) - 1) // len(mods)
+            pace = {"i": 0}
+
+            def pre_hook(mod, inp):
+                j = pace["i"]
+                pace["i"] += 1
+                lo = j * cs
+                if lo < nb:
+                    ls.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(ls):
+                        dst[lo:lo + cs].copy_(src[lo:lo + cs], non_blocking=True)
+            for mm in mods:
+                mm.register_forward_pre_hook(pre_hook)
+            load = (None, None, ls)
+        if arm == "nockpt_d2hload":                 # cost decomposition: the tap's D2H bytes
+            nb = cd.r.padded * 4 // world           # (S/n per iteration) as a plain copy-engine
+            load = (torch.empty(nb, dtype=torch.uint8, device=dev),  # load on its own stream,
+                    torch.empty(nb, dtype=torch.uint8, pin_memory=True),   # no tap, no shadow
+                    torch.cuda.Stream(dev))
 
         def it(i):
             cd.zero_grad()
+            if pace is not None:
+                pace["i"] = 0
+            if load is not None and pace is None:
+                load[2].wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(load[2]):
+                    load[1].copy_(load[0], non_blocking=True)
             with torch.autocast("cuda", dtype=torch.bfloat16):
                 loss = model(tokens[i], labels=tokens[i]).loss
             loss.backward()
             cd.step()
-        streams = [cd.comm, cd.side]
+        streams = [cd.comm, cd.side] + ([load[2]] if load is not None else [])
 
         def cleanup():
             full = not (flags & (cm.CM_FLAG_NO_TAP | cm.CM_FLAG_NO_SHADOW))
@@ -81,9 +118,10 @@ def run_arm(arm, args, rank, world, local):
     b.synchronize()
     ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    drain = cd.r.ctx.info().drain_ctas if arm not in ("nccl",) else None
     ok = cleanup()
     del model
     torch.cuda.empty_cache()
-    return {"ms_per_iter": ms.item(), "shadow_bit_identical": ok}
+    return {"ms_per_iter": ms.item(), "shadow_bit_identical": ok, "drain_ctas": drain}
 
 

@@ -45,6 +45,9 @@ def main():
     ap.add_argument("--arms", default="nccl,ours_nockpt,ours_ckpt")
     ap.add_argument("--tap", default="staged", choices=["staged", "direct", "ce"])
     ap.add_argument("--zero1", action="store_true")
+    ap.add_argument("--drain-ctas", type=int, default=-1,
+                    help="tap drain / persist D2H: -1 library auto policy, 0 copy engine, k > 0 a k-CTA "
+                         "SM drain kernel")
     args = ap.parse_args()
     rank, world, local = setup()
     out = {}
@@ -53,7 +56,8 @@ def main():
     if rank == 0:
         res = {"mode": "model", "model": "GPT-2 small (124M), random init, random tokens", "n_gpus": world,
                "micro_batch": args.micro_batch, "seq_len": 1024, "autocast": "bf16", "persist_every":
-               args.persist_every, "ring_depth": args.ring_depth, "tap": args.tap, "zero1": args.zero1, **out}
+               args.persist_every, "ring_depth": args.ring_depth, "tap": args.tap, "zero1": args.zero1,
+               "drain_ctas": args.drain_ctas, **out}
         if "nccl" in out and "ours_ckpt" in out:
             res["ckpt_overhead_pct_vs_nccl"] = (out["ours_ckpt"]["ms_per_iter"] / out["nccl"]["ms_per_iter"] - 1) * 100
         if "ours_nockpt" in out and "ours_ckpt" in out:
