@@ -46,7 +46,7 @@ constexpr uint32_t kVersion = 1;
 constexpr size_t kAlign = 4096;
 constexpr int kStages = 4;                       // shadow staging buffers
 constexpr int64_t kOsSlotBytes = 1ll << 20;      // one-shot inbox slot (largest one-shot bucket)
-constexpr int64_t kDrainCoalesce = 4ll << 20;    // tap drains of adjacent small shards merge up to this
+constexpr int64_t kDrainCoalesce = 16ll << 20;   // tap drains of adjacent shards merge up to this
 constexpr int64_t kStageElems = 8ll << 20;       // elements per shadow staging chunk
 
 struct SegHeader {
@@ -1514,7 +1514,8 @@ static cm_status ensure_staging(cm_ctx* c) {
 // gradients since it -- every step remains recoverable from host memory alone (restore
 // rolls forward over the ring), with 12/K instead of 12 bytes per element of D2H.
 static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec, cudaStream_t s,
-                                     bool force_persist, bool* persisted, const char* dev_g = nullptr) {
+                                     bool force_persist, bool* persisted, const char* dev_g = nullptr,
+                                     cudaEvent_t grads_consumed = nullptr) {
     const int slot = (int)((step - 1) % c->D);
     const int hin = (int)((step - 1) & 1), hout = (int)(step & 1);
     cm_status st = ensure_staging(c);
@@ -1571,6 +1572,9 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
             }
         }
         CU(cudaEventRecord(c->ev_join, c->cs_k));
+        // the gradients (HBM staging half) are consumed once the kernels are done: the
+        // training stream may reuse the half without waiting for a snapshot persist
+        if (grads_consumed) CU(cudaEventRecord(grads_consumed, c->cs_k));
         CU(cudaStreamWaitEvent(s, c->ev_join, 0));
         if (persist) {
             CU(cudaEventRecord(c->ev_join, c->cs_d2h));
@@ -1607,12 +1611,10 @@ cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
     else CU(cudaStreamWaitEvent(s, c->ev_tap_done[slot], 0));   // all taps of iteration step-1
     bool persisted = false;
     cm_status st = shadow_step_enqueue(c, step, c->slot_sc[slot], s, false, &persisted,
-                                       from_stage ? (const char*)c->stage_buf[h] : nullptr);
+                                       from_stage ? (const char*)c->stage_buf[h] : nullptr,
+                                       from_stage ? c->ev_stage_consumed[h] : nullptr);
     if (st != CM_OK) return st;
-    if (from_stage) {
-        CU(cudaEventRecord(c->ev_stage_consumed[h], s));
-        c->stage_consumer[h] = true;
-    }
+    if (from_stage) c->stage_consumer[h] = true;
     // release ring slots: DEVICE placement once consumed; HOST placement once a persisted
     // snapshot covers them (the ring is the log that makes every step recoverable)
     if (c->shadow_place == CM_SHADOW_DEVICE || persisted) {
