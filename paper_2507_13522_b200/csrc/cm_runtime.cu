@@ -1155,17 +1155,23 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
 // rate), or with drain_ctas > 0 the low-intensity SM drain kernel (host pointer -> its
 // device alias).  Both are stream-ordered like the other, so flags published after it on
 // the same stream follow the data (posted writes stay ordered).
-// Auto policy (drain_ctas = -1): the per-iteration D2H demand (tap S/n + snapshot 12 L / K)
-// over the measured step period.  Below kSmDrainRate the single-CTA SM drain (~11 GB/s) keeps
-// up at a third of its rate or less and the link stays far from saturation; above it the
-// step is link-bound and the copy engine's full rate matters more than interference.
-constexpr double kSmDrainRate = 4.5e9;
+// Auto policy (drain_ctas = -1), from measurements (profiles/r01c_interference.md): a copy
+// engine saturates the device->host link, which slows the GPU's launch-bound work, most when
+// several GPUs share the host's root complex; an SM drain stores at ~11 GB/s per CTA without
+// saturating it but holds SM slots.  Measured best: one GPU -> copy engine (GPT-2: +2.2% vs
+// +5.4% with 2 CTAs); n > 1 -> k = ceil(demand / 5 GB/s) SM drain CTAs, demand = per-step D2H
+// (tap S/n + snapshot 12 L / K) over the measured step period (GPT-2 at n=4: 1 CTA, +1.0% vs
+// +3.3% copy engine; Llama-8B-shaped at n=4: 2 CTAs, -1.9% vs +0.3% vs NCCL); a demand above
+// 4 CTAs (20 GB/s) means the step is link-bound (nothing to hide under) -> copy engine.
+constexpr double kSmDrainPerCta = 5.0e9;
+constexpr int kSmDrainMaxCtas = 4;
 static int drain_ctas_now(const cm_ctx* c) {
     if (c->drain_ctas >= 0) return c->drain_ctas;
-    if (c->iter_period_s <= 0.0) return 0;
+    if (c->n == 1 || c->iter_period_s <= 0.0) return 0;
     double bytes = (double)c->shard_numel * c->es;
     if (c->shadow_place == CM_SHADOW_HOST && !c->no_shadow) bytes += 12.0 * (double)c->shard_numel / c->K;
-    return bytes / c->iter_period_s < kSmDrainRate ? 1 : 0;
+    const int k = (int)std::ceil(bytes / c->iter_period_s / kSmDrainPerCta);
+    return k <= kSmDrainMaxCtas ? std::max(k, 1) : 0;
 }
 
 static cm_status d2h(cm_ctx* c, char* host_dst, const void* dev_src, size_t bytes, cudaStream_t s) {

@@ -102,6 +102,8 @@ def run_arm(arm, args, rank, world, local):
         buckets = R.r.buckets()
         comm = torch.cuda.Stream(dev, priority=-1)
         ctx = R.r.ctx
+        if getattr(args, "drain_ctas", -1) != -1:
+            ctx.set_param("drain_ctas", args.drain_ctas)
 
         def reduce(b, t):
             ev = torch.cuda.Event()
@@ -149,10 +151,11 @@ def run_arm(arm, args, rank, world, local):
     b.synchronize()
     ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    drain = ctx.info().drain_ctas if arm != "nccl" else None
     ok = cleanup()
     gemms = fwd + sum(per)
     return {"ms_per_iter": ms.item(), "shadow_bit_identical": ok, "filler_gemms": gemms,
-            "filler_tflop": gemms * flops / 1e12}
+            "filler_tflop": gemms * flops / 1e12, "drain_ctas": drain}
 
 
 def filler_only_ms(args, local):

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--persist-every", type=int, default=8)
     ap.add_argument("--shadow", default="host", choices=["host", "device"])
     ap.add_argument("--arms", default="nccl,ours_nockpt,ours_ckpt")
+    ap.add_argument("--drain-ctas", type=int, default=-1, help="-1 auto, 0 copy engine, k SM drain CTAs")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -43,7 +44,7 @@ def main():
                                              "fp32 master + AdamW state, ZeRO-1; fwd/bwd replaced by bf16 GEMMs "
                                              "of 6*P*T FLOPs",
                "n_gpus": world, "tokens_per_gpu": args.tokens, "shadow": args.shadow,
-               "ring_depth": args.ring_depth, "persist_every": args.persist_every,
+               "ring_depth": args.ring_depth, "persist_every": args.persist_every, "drain_ctas": args.drain_ctas,
                "filler_only_ms": floor_ms, "filler_tflops": tflops, **out}
         if "nccl" in out and "ours_ckpt" in out:
             res["ckpt_overhead_pct_vs_nccl"] = (out["ours_ckpt"]["ms_per_iter"] / out["nccl"]["ms_per_iter"] - 1) * 100
