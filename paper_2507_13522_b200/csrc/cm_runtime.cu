@@ -1158,20 +1158,24 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
 // Auto policy (drain_ctas = -1), from measurements (profiles/r01c_interference.md): a copy
 // engine saturates the device->host link, which slows the GPU's launch-bound work, most when
 // several GPUs share the host's root complex; an SM drain stores at ~11 GB/s per CTA without
-// saturating it but holds SM slots.  Measured best: one GPU -> copy engine (GPT-2: +2.2% vs
-// +5.4% with 2 CTAs); n > 1 -> k = ceil(demand / 5 GB/s) SM drain CTAs, demand = per-step D2H
-// (tap S/n + snapshot 12 L / K) over the measured step period (GPT-2 at n=4: 1 CTA, +1.0% vs
-// +3.3% copy engine; Llama-8B-shaped at n=4: 2 CTAs, -1.9% vs +0.3% vs NCCL); a demand above
-// 4 CTAs (20 GB/s) means the step is link-bound (nothing to hide under) -> copy engine.
-constexpr double kSmDrainPerCta = 5.0e9;
-constexpr int kSmDrainMaxCtas = 4;
+// saturating it but holds SM slots.  Demand = per-step D2H (tap S/n + snapshot 12 L / K) over
+// the measured step period.  Measured best (GPT-2 model mode, Llama-8B-shaped filler):
+//   one GPU                        -> copy engine  (GPT-2: +2.2% vs NCCL; SM drains +5..+10%)
+//   n > 1, demand <= 2.5 GB/s      -> 1 CTA        (GPT-2 n=4: +0.9%; copy engine +3.3%)
+//   n > 1, demand  > 2.5 GB/s      -> 2 CTAs       (GPT-2 n=2: +1.6%, 1 CTA +3.3%;
+//                                                   Llama n=4: -1.3% vs NCCL, copy engine +0.3%)
+//   demand > 20 GB/s (nothing to hide under: the step is link-bound) -> copy engine
+constexpr double kSmDrainPerCta = 2.5e9;
+constexpr int kSmDrainMaxCtas = 2;
+constexpr double kLinkBoundDemand = 20e9;
 static int drain_ctas_now(const cm_ctx* c) {
     if (c->drain_ctas >= 0) return c->drain_ctas;
     if (c->n == 1 || c->iter_period_s <= 0.0) return 0;
     double bytes = (double)c->shard_numel * c->es;
     if (c->shadow_place == CM_SHADOW_HOST && !c->no_shadow) bytes += 12.0 * (double)c->shard_numel / c->K;
-    const int k = (int)std::ceil(bytes / c->iter_period_s / kSmDrainPerCta);
-    return k <= kSmDrainMaxCtas ? std::max(k, 1) : 0;
+    const double demand = bytes / c->iter_period_s;
+    if (demand > kLinkBoundDemand) return 0;
+    return std::min(kSmDrainMaxCtas, std::max(1, (int)std::ceil(demand / kSmDrainPerCta)));
 }
 
 static cm_status d2h(cm_ctx* c, char* host_dst, const void* dev_src, size_t bytes, cudaStream_t s) {

@@ -8,3 +8,4 @@ timeout 600 $RUN tools/model_mode.py --steps 20 --warmup 5 --arms nccl,ours_nock
 for k in 1 2 4; do
   timeout 400 $RUN tools/model_mode.py --steps 20 --warmup 5 --arms ours_tap_only,ours_ckpt --drain-ctas $k >> $F 2>> $OUT/${TAG}_drain_n$N.err
 done
+timeout 600 $RUN tools/model_mode.py --steps 20 --warmup 5 --arms nccl,ours_ckpt >> $F 2>> $OUT/${TAG}_drain_n$N.err
