@@ -210,6 +210,7 @@ struct ArParams {
     uint32_t epoch;
     int rank;
     int barriers;           // 0 when all ranks live in this process (virtual ranks)
+    int exit_barrier;       // 0: the iteration's fence is the training step's entry barrier
     int ag;                 // 0 when n == 1 (the reduced value equals the local value)
     unsigned long long* done_ctr;  // device counter: last block to finish publishes the flag
     unsigned long long done_target;
@@ -299,7 +300,9 @@ __global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P)
             }
         }
     }
-    if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 1);   // bucket complete everywhere
+    // bucket complete everywhere; skipped when the training step's entry barrier fences the
+    // whole iteration instead (the next bucket's kernel then overlaps this one's store tail)
+    if (P.barriers && P.exit_barrier) block_barrier(P.pads, N, P.rank, P.epoch, 1);
 }
 
 // ------------------------------------------------------------------ one-shot push AR
@@ -427,6 +430,14 @@ struct AdamParams {
     float rec[10];                 // the record's scalars (AdamScalars or SgdScalars)
     int32_t rec_kind;
     int64_t step;
+    // iteration fence (training step only, multi-process, lazy all-reduce exits): block j
+    // waits for block j of every rank, i.e. for every rank to have finished ALL its
+    // all-reduce kernels of the iteration -- their all-gather stores into this rank's grad
+    // buffer have landed, and nobody still reads this rank's grads when the next backward
+    // overwrites them
+    Pads pads;
+    uint32_t epoch;
+    int fence_n, fence_rank;       // fence_n = 0: no fence
 };
 
 // the step's scalars into the host-mapped ring-slot record, then its tag (one thread)
@@ -536,6 +547,7 @@ __device__ __forceinline__ void wt_compute_store(const AdamParams& P, int64_t e,
 
 template <typename G, int OPT>
 __device__ __forceinline__ void wt_body(const AdamParams& P) {
+    if (P.fence_n) block_barrier(P.pads, P.fence_n, P.fence_rank, P.epoch, 0);
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)kAdamThreads + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kAdamThreads) >> 5;

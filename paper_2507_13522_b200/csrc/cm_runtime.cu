@@ -165,6 +165,8 @@ struct cm_ctx {
     size_t mc_size = 0;
     int64_t oneshot_max = 0;              // buckets <= this many bytes use the one-shot kernel
     bool ablate_no_drain = false;         // ablation only: staged taps never reach the host ring
+    bool lazy_exit = true;                // all-reduce kernels without exit barrier; the training
+                                          // step's entry barrier fences the iteration instead
     int drain_ctas = -1;                  // D2H of tap drains / persists: 0 copy engine, k>0 k-CTA SM
                                           // drain, -1 auto (SM drain when the link demand is low)
     double iter_period_s = 0.0;           // EMA of the host period between training steps
@@ -415,14 +417,14 @@ static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaSt
         const int grid = (int)std::min<int64_t>(want, std::min(blocks, c->wt_blocks));
         if (c->dtype == CM_F32) sgd_wt_kernel<F32Tag><<<grid, kAdamThreads, 0, s>>>(P);
         else sgd_wt_kernel<BF16Tag><<<grid, kAdamThreads, 0, s>>>(P);
-    } else if (c->adamw_impl == 1) {
+    } else if (c->adamw_impl == 1 && !P.fence_n) {   // (the iteration fence lives in the warp-tiled body)
         const int64_t tiles = (P.n + kTmaTile - 1) / kTmaTile;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->tma_blocks));
         if (c->dtype == CM_F32)
             adamw_tma_kernel<F32Tag><<<grid, kTmaThreads, kTmaStages * TmaTile<F32Tag>::kStageBytes, s>>>(P);
         else
             adamw_tma_kernel<BF16Tag><<<grid, kTmaThreads, kTmaStages * TmaTile<BF16Tag>::kStageBytes, s>>>(P);
-    } else if (c->adamw_impl == 2) {
+    } else if (c->adamw_impl == 2 || P.fence_n) {
         const int64_t tiles = P.n / kWarpTile;
         const int64_t want = std::max<int64_t>(1, (tiles + kAdamThreads / 32 - 1) / (kAdamThreads / 32));
         const int grid = (int)std::min<int64_t>(want, std::min(blocks, c->wt_blocks));
@@ -551,6 +553,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "ar_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_max = (int)value;
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
+    else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
     // cost decomposition only (tools/model_mode.py): the staged tap's copy-engine drain is not
     // issued, so the ring is never written -- restore and the host-ring fallback are invalid
     else if (k == "ablate_no_drain" && (value == 0 || value == 1) && c->no_shadow) c->ablate_no_drain = value;
@@ -1260,6 +1263,9 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     P.rank = c->rank;
     P.barriers = c->barriers ? 1 : 0;
     P.ag = (c->n > 1 && !c->zero1) ? 1 : 0;   // ZeRO-1 gathers the updated params instead
+    // exit barrier only when the training step does not fence the iteration: ZeRO-1's
+    // optimizer ends in a barrier; the replicated AdamW starts with one when lazy_exit
+    P.exit_barrier = (c->lazy_exit || c->zero1) ? 0 : 1;
     // tap modes: fused (kernel stores to the host ring), staged (kernel stores to an HBM
     // staging half, a copy engine drains it to the ring), copy-engine (CE reads the reduced
     // shard back from the grad buffer after the kernel)
@@ -1480,6 +1486,12 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
         cudaError_t e = cudaGetLastError();
         st = e == cudaSuccess ? CM_OK : fail(c, CM_ERR_CUDA, "zero1 launch: %s", cudaGetErrorString(e));
     } else {
+        if (c->barriers && c->n > 1 && c->lazy_exit) {
+            P.pads = c->pads;
+            P.epoch = ++c->epoch;
+            P.fence_n = c->n;
+            P.fence_rank = c->rank;
+        }
         TimedScope ts(c, 1, S(stream));
         st = launch_adamw(c, P, c->adam_blocks, S(stream));
     }

@@ -596,3 +596,39 @@ def test_checkpoint_file_save_load_restore(tmp_path):
             assert r.ctx.verify(g2.stream) == -1
     finally:
         close(g2)
+
+
+@pytest.mark.parametrize("drain", [0, 1, 2])
+def test_drain_modes_ring_and_restore_bit_exact(drain):
+    """The tap drain and the snapshot persist by copy engine (0) or by the SM drain kernel
+    (1, 2 CTAs): the ring holds T exactly, the host snapshot equals the shadow, and a restore
+    that rolls forward over the ring resumes bit-exact."""
+    numel = TABLES["ragged"]
+    n, K, D = 2, 4, 4
+    name = _name()
+    g = harness.VirtualGroup(numel, n, 0, cm.CM_F32, 1 << 20, name, D, cm.CM_SHADOW_HOST, 0, 0, persist_every=K)
+    g._shm = name
+    for r in g.ranks:
+        r.ctx.set_param("drain_ctas", drain)
+    plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
+    try:
+        kill_at = 2 * K + 1
+        for t in range(kill_at):
+            g.step()
+            ref.step()
+            g.sync()
+            for r in g.ranks:
+                r.ctx.join(g.stream)
+            g.stream.synchronize()
+            np.testing.assert_array_equal(bits(ring_flat(g, t % D)), bits(ref.T), err_msg=f"ring t {t}")
+            assert all(r.ctx.info().drain_ctas == drain for r in g.ranks)
+        for r in g.ranks:
+            assert r.ctx.verify(g.stream) == -1
+            r.p.fill_(float("nan")); r.m.fill_(float("nan")); r.v.fill_(float("nan"))
+        torch.cuda.synchronize()
+        assert [r.ctx.restore(g.stream) for r in g.ranks] == [kill_at] * n
+        for r in g.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            np.testing.assert_array_equal(bits(t2np(r.v)), bits(ref.v))
+    finally:
+        close(g)
