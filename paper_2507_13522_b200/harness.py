@@ -43,6 +43,11 @@ class Rank:
         self.ctx = cm.Context(world_size, rank, device, ring_depth, shadow_place, shm_name, flags, persist_every)
         self.blob = self.ctx.register_buckets(self.numel, grad_dtype, cap_bytes, self.grad.data_ptr(),
                                               self.p.data_ptr(), self.m.data_ptr(), self.v.data_ptr())
+        # A/B switches for tools (collective settings: every rank must use the same value)
+        for key in ("lazy_exit", "drain_ctas", "oneshot_max_bytes"):
+            val = os.environ.get("CM_" + key.upper())
+            if val is not None:
+                self.ctx.set_param(key, int(val))
         if init_state:
             with torch.cuda.device(dev):
                 s = torch.cuda.current_stream(dev)
