@@ -325,6 +325,9 @@ struct OsParams {
     char* mc;                      // NVLS: multicast address of slot [rank] (nullptr: unicast)
     int64_t nvec;                  // 16-byte vectors in the bucket
     int64_t shard_lo, shard_hi;    // this rank's shard, in vectors
+    int64_t shard_vec;             // vectors per shard (E_b / n * sizeof(G) / 16)
+    int rs_only;                   // ZeRO-1: push shard k to rank k only, reduce the own shard
+                                   // into the tap target, leave the grad buffer untouched
     Pads pads;
     uint32_t epoch;
     int rank;
@@ -340,7 +343,12 @@ template <typename G, int N>
 __global__ void __launch_bounds__(kOsThreads) os_tap_kernel(const OsParams P) {
     const int64_t stride = (int64_t)gridDim.x * kOsThreads;
     const int64_t q0 = blockIdx.x * (int64_t)kOsThreads + threadIdx.x;
-    if (P.mc) {                                              // push once: the switch replicates
+    if (P.rs_only) {                                         // push shard k to its owner only
+        for (int64_t q = q0; q < P.nvec; q += stride) {
+            const int k = (int)(q / P.shard_vec);
+            if (k != P.rank) st_v4(P.push[k] + q * 16, ld_v4(P.own + q * 16));
+        }
+    } else if (P.mc) {                                       // push once: the switch replicates
         for (int64_t q = q0; q < P.nvec; q += stride) mc_st_v4(P.mc + q * 16, ld_v4(P.own + q * 16));
         __threadfence_system();
     } else {                                                 // push n-1 unicast copies
@@ -353,11 +361,12 @@ __global__ void __launch_bounds__(kOsThreads) os_tap_kernel(const OsParams P) {
     }
     block_barrier(P.pads, N, P.rank, P.epoch, 0);            // every rank's chunk arrived
     for (int64_t q = q0; q < P.nvec; q += stride) {          // reduce from the local inbox
+        if (P.rs_only && (q < P.shard_lo || q >= P.shard_hi)) continue;
         uint4 x[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) x[k] = ld_v4((k == P.rank ? (const char*)P.own : P.inbox[k]) + q * 16);
         const uint4 r = reduce_vec<G, N>(x);
-        st_v4(P.own + q * 16, r);
+        if (!P.rs_only) st_v4(P.own + q * 16, r);
         if (P.tap && q >= P.shard_lo && q < P.shard_hi) st_cs_v4(P.tap + (q - P.shard_lo) * 16, r);
     }
     if (P.tap_flag) {

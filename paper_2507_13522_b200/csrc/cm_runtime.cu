@@ -1306,7 +1306,9 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     // small buckets take the one-shot push kernel (multi-process ranks only:
     // virtual ranks share one stream, where a rank cannot wait for its peers' pushes;
     // they use the two-shot kernel, which computes the same rank-order sum)
-    const bool oneshot = c->n > 1 && c->barriers && !c->zero1 && B.padded * c->es <= c->oneshot_max;
+    // (ZeRO-1: the push reduce-scatter variant -- shard k goes to rank k only, no all-gather;
+    // the NVLS multicast push is for the all-reduce form only)
+    const bool oneshot = c->n > 1 && c->barriers && B.padded * c->es <= c->oneshot_max;
     if (oneshot && !skip_kernel) {
         OsParams O{};
         const int64_t bucket_bytes = B.padded * c->es;
@@ -1317,11 +1319,13 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
             const char* in = c->nvls ? (const char*)c->uc_va : c->inbox;
             O.inbox[k] = in + ((size_t)h * c->n + k) * kOsSlotBytes;
         }
-        if (c->nvls) O.mc = (char*)c->mc_va + ((size_t)h * c->n + c->rank) * kOsSlotBytes;
+        if (c->nvls && !c->zero1) O.mc = (char*)c->mc_va + ((size_t)h * c->n + c->rank) * kOsSlotBytes;
         O.tap = P.tap;
         O.nvec = bucket_bytes / 16;
         O.shard_lo = (int64_t)c->rank * (shard * c->es / 16);
         O.shard_hi = O.shard_lo + shard * c->es / 16;
+        O.shard_vec = shard * c->es / 16;
+        O.rs_only = c->zero1 ? 1 : 0;
         O.pads = c->pads;
         O.epoch = P.epoch;
         O.rank = c->rank;

@@ -4,7 +4,7 @@ real NVLink peer memory and checks its own state bit-for-bit against the oracle.
 
   python -m torch.distributed.run --nproc-per-node N tests/mp_worker.py <mode> <name>
 modes: parity_f32, parity_bf16, parity_zero1, parity_sgd, parity_oneshot, parity_oneshot_bf16,
-       parity_oneshot_direct, parity_nvls, parity_nvls_bf16, restore_soft, hardkill_phase1, hardkill_phase2
+       parity_oneshot_direct, parity_nvls, parity_nvls_bf16, parity_zero1_oneshot, restore_soft, hardkill_phase1, hardkill_phase2
 """
 import os
 import sys
@@ -69,14 +69,14 @@ def main():
         if opt == "sgd" else HP_O
     ref = O.Run(plan, seed=0, dtype=dtype, gscale=W.GRAD_SCALE, hp=hp_o, opt=opt)
     flags = cm.CM_FLAG_ATTACH if mode == "hardkill_phase2" else 0
-    if mode == "parity_zero1":
+    if mode.startswith("parity_zero1"):
         flags |= cm.CM_FLAG_ZERO1
     if mode == "parity_oneshot_direct":
         flags |= cm.CM_FLAG_TAP_DIRECT
     if mode.startswith("parity_nvls"):
         flags |= cm.CM_FLAG_NVLS
     R = harness.DistRank(numel, dtype, cap, name, 2, cm.CM_SHADOW_HOST, flags, opt=opt)
-    if mode.startswith("parity_oneshot") or mode.startswith("parity_nvls"):
+    if mode.startswith("parity_oneshot") or mode.startswith("parity_nvls") or mode == "parity_zero1_oneshot":
         # buckets up to 512 KiB / 1 MiB take the one-shot push kernel, the rest
         # the two-shot kernel; both must give the oracle's bits
         R.r.ctx.set_param("oneshot_max_bytes", (1 << 20) if "bf16" in mode else (512 << 10))
@@ -85,7 +85,7 @@ def main():
             R.step()
             ref.step()
             R.sync()
-            check(R, ref, f"iteration {t}", plan if mode == "parity_zero1" else None)
+            check(R, ref, f"iteration {t}", plan if mode.startswith("parity_zero1") else None)
     elif mode == "restore_soft":
         for _ in range(4):
             R.step()

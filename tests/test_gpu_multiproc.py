@@ -27,7 +27,7 @@ def counts():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("mode", ["parity_f32", "parity_bf16", "parity_zero1", "parity_sgd",
                                   "parity_oneshot", "parity_oneshot_bf16", "parity_oneshot_direct",
-                                  "parity_nvls", "parity_nvls_bf16",
+                                  "parity_nvls", "parity_nvls_bf16", "parity_zero1_oneshot",
                                   "restore_soft"])
 def test_multiprocess(mode):
     for n in counts():
