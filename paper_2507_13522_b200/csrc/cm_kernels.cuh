@@ -253,40 +253,23 @@ constexpr int kArThreads = 512;
 constexpr int kArUnroll = 2;
 
 template <typename G, int N>
-__global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P) {
-    if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 0);   // peers' grads are ready
-
-    const int64_t stride = (int64_t)gridDim.x * kArThreads;
-    int64_t q = blockIdx.x * (int64_t)kArThreads + threadIdx.x;
-    for (; q + (kArUnroll - 1) * stride < P.nvec; q += kArUnroll * stride) {
-        uint4 x[kArUnroll][N];
+__device__ __forceinline__ void ar_load(const ArParams& P, int64_t q, uint4 (&x)[N]) {
 #pragma unroll
-        for (int u = 0; u < kArUnroll; ++u)
+    for (int k = 0; k < N; ++k) x[k] = ld_v4(P.buf[k] + q * 16);
+}
+template <typename G, int N>
+__device__ __forceinline__ void ar_reduce_store(const ArParams& P, int64_t q, const uint4 (&x)[N]) {
+    const uint4 r = reduce_vec<G, N>(x);
+    const int64_t off = q * 16;
+    if (P.tap) st_cs_v4(P.tap + off, r);
+    if (P.ag) {
 #pragma unroll
-            for (int k = 0; k < N; ++k) x[u][k] = ld_v4(P.buf[k] + (q + u * stride) * 16);
-#pragma unroll
-        for (int u = 0; u < kArUnroll; ++u) {
-            const uint4 r = reduce_vec<G, N>(x[u]);
-            const int64_t off = (q + u * stride) * 16;
-            if (P.tap) st_cs_v4(P.tap + off, r);
-            if (P.ag) {
-#pragma unroll
-                for (int k = 0; k < N; ++k) st_v4(P.buf[k] + off, r);
-            }
-        }
+        for (int k = 0; k < N; ++k) st_v4(P.buf[k] + off, r);
     }
-    for (; q < P.nvec; q += stride) {
-        uint4 x[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) x[k] = ld_v4(P.buf[k] + q * 16);
-        const uint4 r = reduce_vec<G, N>(x);
-        if (P.tap) st_cs_v4(P.tap + q * 16, r);
-        if (P.ag) {
-#pragma unroll
-            for (int k = 0; k < N; ++k) st_v4(P.buf[k] + q * 16, r);
-        }
-    }
-
+}
+// tap flag of the direct tap (last block publishes) and the optional exit barrier
+template <int N>
+__device__ __forceinline__ void ar_epilogue(const ArParams& P) {
     if (P.tap_flag) {
         // every tap store of this block is visible system-wide before the block is
         // counted; the last block publishes the (slot, bucket, rank) flag for restore
@@ -303,6 +286,51 @@ __global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P)
     // bucket complete everywhere; skipped when the training step's entry barrier fences the
     // whole iteration instead (the next bucket's kernel then overlaps this one's store tail)
     if (P.barriers && P.exit_barrier) block_barrier(P.pads, N, P.rank, P.epoch, 1);
+}
+
+template <typename G, int N>
+__global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P) {
+    if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 0);   // peers' grads are ready
+
+    const int64_t stride = (int64_t)gridDim.x * kArThreads;
+    int64_t q = blockIdx.x * (int64_t)kArThreads + threadIdx.x;
+    for (; q + (kArUnroll - 1) * stride < P.nvec; q += kArUnroll * stride) {
+        uint4 x[kArUnroll][N];
+#pragma unroll
+        for (int u = 0; u < kArUnroll; ++u) ar_load<G, N>(P, q + u * stride, x[u]);
+#pragma unroll
+        for (int u = 0; u < kArUnroll; ++u) ar_reduce_store<G, N>(P, q + u * stride, x[u]);
+    }
+    for (; q < P.nvec; q += stride) {
+        uint4 x[N];
+        ar_load<G, N>(P, q, x);
+        ar_reduce_store<G, N>(P, q, x);
+    }
+    ar_epilogue<N>(P);
+}
+
+// Software-pipelined variant (cm_set_param("ar_impl", 1)): one block per SM, each thread
+// walks its vectors with the n loads of vector q + stride in flight while vector q is
+// reduced and stored, so the inbound (reads) and outbound (all-gather stores) directions
+// of the links are busy at the same time instead of in alternating phases.
+template <typename G, int N>
+__global__ void __launch_bounds__(kArThreads, 1) rs_tap_ag_pipe_kernel(const ArParams P) {
+    if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 0);   // peers' grads are ready
+    const int64_t stride = (int64_t)gridDim.x * kArThreads;
+    int64_t q = blockIdx.x * (int64_t)kArThreads + threadIdx.x;
+    if (q < P.nvec) {
+        uint4 cur[N];
+        ar_load<G, N>(P, q, cur);
+        for (; q < P.nvec; q += stride) {
+            uint4 nxt[N];
+            const int64_t qn = q + stride;
+            if (qn < P.nvec) ar_load<G, N>(P, qn, nxt);
+            ar_reduce_store<G, N>(P, q, cur);
+#pragma unroll
+            for (int k = 0; k < N; ++k) cur[k] = nxt[k];
+        }
+    }
+    ar_epilogue<N>(P);
 }
 
 // ------------------------------------------------------------------ one-shot push AR

@@ -187,6 +187,8 @@ struct cm_ctx {
     int ar_blocks_max = 296, adam_blocks = 1184, shadow_blocks = 296, misc_blocks = 1184;
     int ar_blocks_tap_only = 32;   // n == 1: the kernel is only the PCIe tap; leave SMs free
     int adamw_impl = 2;            // 0 vectorised, 1 TMA bulk-copy staged, 2 warp-tiled (measured best)
+    int ar_impl = 0;               // 0 unrolled two-shot, 1 software-pipelined (one block per SM)
+    int ar_pipe_blocks = 148;
     int tma_blocks = 148;
     int wt_blocks = 296;
 
@@ -383,6 +385,20 @@ static int ar_occupancy(int n) {
 }
 
 template <typename G>
+static void launch_ar_pipe_t(int n, dim3 grid, cudaStream_t s, const ArParams& P) {
+    switch (n) {
+        case 1: rs_tap_ag_pipe_kernel<G, 1><<<grid, kArThreads, 0, s>>>(P); break;
+        case 2: rs_tap_ag_pipe_kernel<G, 2><<<grid, kArThreads, 0, s>>>(P); break;
+        case 3: rs_tap_ag_pipe_kernel<G, 3><<<grid, kArThreads, 0, s>>>(P); break;
+        case 4: rs_tap_ag_pipe_kernel<G, 4><<<grid, kArThreads, 0, s>>>(P); break;
+        case 5: rs_tap_ag_pipe_kernel<G, 5><<<grid, kArThreads, 0, s>>>(P); break;
+        case 6: rs_tap_ag_pipe_kernel<G, 6><<<grid, kArThreads, 0, s>>>(P); break;
+        case 7: rs_tap_ag_pipe_kernel<G, 7><<<grid, kArThreads, 0, s>>>(P); break;
+        default: rs_tap_ag_pipe_kernel<G, 8><<<grid, kArThreads, 0, s>>>(P); break;
+    }
+}
+
+template <typename G>
 static void launch_ar_t(int n, dim3 grid, cudaStream_t s, const ArParams& P) {
     switch (n) {
         case 1: rs_tap_ag_kernel<G, 1><<<grid, kArThreads, 0, s>>>(P); break;
@@ -554,6 +570,8 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
     else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
+    else if (k == "ar_impl" && (value == 0 || value == 1)) c->ar_impl = (int)value;
+    else if (k == "ar_pipe_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_pipe_blocks = (int)value;
     // cost decomposition only (tools/model_mode.py): the staged tap's copy-engine drain is not
     // issued, so the ring is never written -- restore and the host-ring fallback are invalid
     else if (k == "ablate_no_drain" && (value == 0 || value == 1) && c->no_shadow) c->ablate_no_drain = value;
@@ -1345,8 +1363,21 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         CHECK_LAUNCH();
     } else if (!skip_kernel) {
         TimedScope ts(c, 0, s);
-        if (c->dtype == CM_F32) launch_ar_t<F32Tag>(c->n, grid, s, P);
-        else launch_ar_t<BF16Tag>(c->n, grid, s, P);
+        if (c->ar_impl == 1) {
+            // one block per SM (co-resident by construction); the done counter of a direct
+            // tap was advanced by `grid` above, re-base it on this grid
+            const int pg = (int)std::max<int64_t>(1, std::min<int64_t>(
+                (P.nvec + kArThreads - 1) / kArThreads, std::min(c->ar_pipe_blocks, c->sms)));
+            if (fused_tap) {
+                c->done_total += (unsigned long long)pg - (unsigned long long)grid;
+                P.done_target = c->done_total;
+            }
+            if (c->dtype == CM_F32) launch_ar_pipe_t<F32Tag>(c->n, pg, s, P);
+            else launch_ar_pipe_t<BF16Tag>(c->n, pg, s, P);
+        } else {
+            if (c->dtype == CM_F32) launch_ar_t<F32Tag>(c->n, grid, s, P);
+            else launch_ar_t<BF16Tag>(c->n, grid, s, P);
+        }
         c->launches++;
         CHECK_LAUNCH();
     }

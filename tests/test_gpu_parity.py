@@ -632,3 +632,27 @@ def test_drain_modes_ring_and_restore_bit_exact(drain):
             np.testing.assert_array_equal(bits(t2np(r.v)), bits(ref.v))
     finally:
         close(g)
+
+
+@pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_pipelined_allreduce_kernel_bit_exact(n, dtype):
+    """ar_impl=1 (software-pipelined two-shot kernel, one block per SM): same bits."""
+    numel = TABLES["mixed"]
+    g = make_group(numel, n, dtype)
+    for r in g.ranks:
+        r.ctx.set_param("ar_impl", 1)
+        r.ctx.set_param("ar_pipe_blocks", 7)      # several vectors per thread on these sizes
+    plan, ref = oracle_for(numel, n, dtype, 1 << 20)
+    try:
+        for t in range(3):
+            g.step()
+            ref.step()
+            g.sync()
+            for r in g.ranks:
+                np.testing.assert_array_equal(bits(t2np(r.grad)), bits(ref.R), err_msg=f"R rank {r.rank} t {t}")
+                np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+                assert r.ctx.verify(g.stream) == -1
+            np.testing.assert_array_equal(bits(ring_flat(g, t % 2)), bits(ref.T), err_msg=f"tap t {t}")
+    finally:
+        close(g)
