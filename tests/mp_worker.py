@@ -54,12 +54,56 @@ def check(R, ref, what, plan=None):
     assert r.ctx.verify(R.stream) == -1, f"{what}: shadow != train on rank {R.rank_id}"
 
 
+def llama_full_zero1(name):
+    """BASELINE.json configs[3] at full size: Llama-3-8B-shaped (8.03 B params, 226 buckets,
+    bf16 grads) ZeRO-1 with the host shadow, 3 iterations; every rank's full p and its
+    shard-local m, v compared with the oracle's per-element trajectories on sampled indices
+    (PAPER.md:306-308 element independence), plus the shadow verify."""
+    n, rank = dist.get_world_size(), dist.get_rank()
+    numel = W.numels(W.llama3_8b())
+    R = harness.DistRank(numel, cm.CM_BF16, W.CAP_BYTES, name, 4, cm.CM_SHADOW_HOST, cm.CM_FLAG_ZERO1,
+                         persist_every=2)
+    steps = 3
+    for _ in range(steps):
+        R.step()
+    R.sync()
+    assert R.r.ctx.verify(R.stream) == -1
+    plan = O.Plan(numel, W.CAP_BYTES, 2, n)
+    rng = np.random.default_rng(rank)
+    idx = rng.choice(plan.total, 1 << 14, replace=False)
+    edges = np.concatenate([plan.bucket_off, plan.bucket_off + plan.bucket_padded - 1])
+    idx = np.unique(np.concatenate([idx, edges])).astype(np.int64)
+    bi = np.searchsorted(plan.bucket_off, idx, side="right") - 1
+    used = ((idx - plan.bucket_off[bi]) < plan.bucket_used[bi]).astype(np.uint8)   # no 8 GB mask
+    p, m, v, _ = O.run_sample(W.SEED, n, O.BF16, W.GRAD_SCALE, steps, idx, used, **HP_O)
+    ti = torch.from_numpy(idx).to(R.r.p.device)
+    np.testing.assert_array_equal(bits(R.r.p[ti].cpu().numpy()), bits(p), err_msg=f"p rank {rank}")
+    # shard-local m, v: flat i in bucket b, shard r -> shard_off_b + (i - off_b - r E_b/n)
+    b = np.searchsorted(plan.bucket_off, idx, side="right") - 1
+    e = plan.bucket_padded[b] // n
+    local = idx - plan.bucket_off[b] - rank * e
+    mine = (local >= 0) & (local < e)
+    j = (plan.bucket_off[b] // n + local)[mine]
+    tj = torch.from_numpy(j).to(R.r.m.device)
+    np.testing.assert_array_equal(bits(R.r.m[tj].cpu().numpy()), bits(m[mine]), err_msg=f"m rank {rank}")
+    np.testing.assert_array_equal(bits(R.r.v[tj].cpu().numpy()), bits(v[mine]), err_msg=f"v rank {rank}")
+    return R, int(mine.sum())
+
+
 def main():
     mode, name = sys.argv[1], sys.argv[2]
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = dist.get_world_size()
+    if mode == "llama_full_zero1":
+        R, k = llama_full_zero1(name)
+        dist.barrier()
+        R.r.ctx.finalize()
+        cm.unlink_shadow(name, R.rank_id)
+        dist.destroy_process_group()
+        print(f"rank {R.rank_id}: {mode} ok ({k} sampled shard elements)", flush=True)
+        return
     dtype = cm.CM_BF16 if mode.endswith("bf16") else cm.CM_F32
     numel = W.numels(W.c1_ragged()) + [5, 70001]
     cap = 1 << 20

@@ -48,3 +48,14 @@ def test_hard_kill_restore():
     p = launch(n, "hardkill_phase2", name)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert p.stdout.count("hardkill_phase2 ok") == n
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs >= 4 GPUs (8 B params of ZeRO-1 state + shadow per GPU)")
+def test_llama8b_full_size_zero1_sampled():
+    """BASELINE.json configs[3] (Llama-3-8B-shaped, bf16 grads, fp32 AdamW, host shadow) at
+    full size in the bench's launch configuration (ZeRO-1, one process per GPU): sampled
+    elements of every rank's state bit-exact vs the oracle after 3 iterations."""
+    name = f"cmll{os.getpid()}"
+    p = launch(4, "llama_full_zero1", name, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert p.stdout.count("llama_full_zero1 ok") == 4
