@@ -175,6 +175,29 @@ def host_link_peaks(dev):
         b.record()
         torch.cuda.synchronize()
         out[name] = 5 * n / (a.elapsed_time(b) * 1e-3) / 1e9
+    # the same D2H into memory like the shadow segment's (a shared mmap registered with
+    # cudaHostRegister, 4 KiB pages) -- what the tap drains and persists actually write to
+    try:
+        import ctypes
+        import mmap
+        mm = mmap.mmap(-1, n, flags=mmap.MAP_SHARED | mmap.MAP_ANONYMOUS)
+        hreg = torch.frombuffer(mm, dtype=torch.uint8)
+        hreg.fill_(0)
+        if torch.cuda.cudart().cudaHostRegister(hreg.data_ptr(), n, 0) == 0:
+            for _ in range(2):
+                hreg.copy_(d, non_blocking=True)
+            torch.cuda.synchronize()
+            a.record()
+            for _ in range(5):
+                hreg.copy_(d, non_blocking=True)
+            b.record()
+            torch.cuda.synchronize()
+            out["d2h_registered"] = 5 * n / (a.elapsed_time(b) * 1e-3) / 1e9
+            torch.cuda.cudart().cudaHostUnregister(hreg.data_ptr())
+        del hreg
+        mm.close()
+    except Exception:   # noqa: BLE001 -- a measurement aid; the roofline uses d2h
+        pass
     return out
 
 
