@@ -288,6 +288,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     iters_per_s = 1000.0 / ms_step
     # bit-identity of the shadow after the timed run (verify synchronises)
     mismatch = ctx.verify(R.stream)
+    iso_ms, iso_cnt = isolated_kernels(args, dtype, cap, numel)
 
     # ----- per-kernel rooflines (average launch duration, live events on each kernel's stream)
     # and the step's binding resource.  Algorithmic bytes per unit are in DESIGN.md 6.
@@ -321,6 +322,14 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
                    bytes_per_launch=ar_hbm, peak_source=hbm_src)
     ent["frac"] = ent["achieved"] / ent["peak"]
     kern["rs_tap_ag"] = ent
+    if iso_cnt[0]:
+        iso_ar = max_over_ranks(iso_ms[0] / iso_cnt[0])
+        b_ar = ent["bytes_per_launch"]
+        kern["rs_tap_ag_isolated"] = {"avg_ms": iso_ar, "launches": iso_cnt[0], "bound": ent["bound"],
+                                      "achieved": b_ar / (iso_ar * 1e-3) / 1e9, "peak": ent["peak"],
+                                      "unit": ent["unit"], "bytes_per_launch": b_ar,
+                                      "frac": b_ar / (iso_ar * 1e-3) / 1e9 / ent["peak"],
+                                      "what": "same kernel timed on its own: staged tap to HBM, no shadow, no device->host drain"}
     ad_ms = kms[1] / max(kcnt[1], 1)
     if args.zero1:
         # sharded AdamW on L = P/n elements, fused with the parameter all-gather: HBM es+24
@@ -342,6 +351,13 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
                               "achieved": ad_bytes / (ad_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                               "bytes_per_launch": ad_bytes, "peak_source": hbm_src}
         kern["adamw_step"]["frac"] = kern["adamw_step"]["achieved"] / hbm_peak
+        if iso_cnt[1]:
+            iso_ad = max_over_ranks(iso_ms[1] / iso_cnt[1])
+            kern["adamw_step_isolated"] = {"avg_ms": iso_ad, "launches": iso_cnt[1], "bound": "hbm",
+                                           "achieved": ad_bytes / (iso_ad * 1e-3) / 1e9, "peak": hbm_peak,
+                                           "unit": "GB/s", "bytes_per_launch": ad_bytes,
+                                           "frac": ad_bytes / (iso_ad * 1e-3) / 1e9 / hbm_peak,
+                                           "what": "same kernel timed on its own: staged tap to HBM, no shadow, no device->host drain"}
     sh_ms = kms[2] / max(kcnt[2], 1)
     sh_hbm = L * (es + 24)
     sh_d2h = L * 12 / K if place == cm.CM_SHADOW_HOST else 0.0
@@ -395,6 +411,35 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
         if r == rank:
             cm.unlink_shadow(shm, r)
     return result
+
+
+def isolated_kernels(args, dtype, cap, numel):
+    """The all-reduce (+ staged tap) and AdamW kernels timed on their own: a second context
+    with the tap's HBM staging stores but no shadow and no device->host drain
+    (CM_FLAG_NO_SHADOW + ablate_no_drain).  In the checkpointed step a saturated
+    device->host link delays the GPU's command fetch (profiles/r01c_interference.md), and
+    short kernels' event-timed durations absorb that delay; this pass gives the kernels'
+    own rooflines.  Skipped for Llama (no HBM for a second set of buffers)."""
+    import torch.distributed as dist
+    from paper_2507_13522_b200 import cm, harness
+    if args.workload == "llama8b":
+        return [0.0] * 5, [0] * 5
+    flags = cm.CM_FLAG_NO_SHADOW | (cm.CM_FLAG_ZERO1 if args.zero1 else 0)
+    name = f"cmiso_{os.environ.get('MASTER_PORT', '0')}_{os.getpid()}"
+    R = harness.DistRank(numel, dtype, cap, name, 2, cm.CM_SHADOW_HOST, flags)
+    R.r.ctx.set_param("ablate_no_drain", 1)
+    for _ in range(3):
+        R.step(shadow=False)
+    R.sync()
+    dist.barrier()
+    R.r.ctx.timing(True)
+    for _ in range(5):
+        R.step(shadow=False)
+    R.sync()
+    ms, cnt = R.r.ctx.timing(False)
+    R.r.ctx.finalize()
+    cm.unlink_shadow(name, dist.get_rank())
+    return ms, cnt
 
 
 def run_e2e(args, R, S_bytes, es):
