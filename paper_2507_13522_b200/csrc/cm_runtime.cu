@@ -46,7 +46,7 @@ constexpr uint32_t kVersion = 1;
 constexpr size_t kAlign = 4096;
 constexpr int kStages = 4;                       // shadow staging buffers
 constexpr int64_t kOsSlotBytes = 1ll << 20;      // one-shot inbox slot (largest one-shot bucket)
-constexpr int64_t kDrainCoalesce = 16ll << 20;   // tap drains of adjacent shards merge up to this
+constexpr int64_t kDrainCoalesce = 64ll << 20;   // tap drains of adjacent shards merge up to this
 constexpr int64_t kStageElems = 8ll << 20;       // elements per shadow staging chunk
 
 struct SegHeader {
@@ -1213,9 +1213,11 @@ static cm_status d2h(cm_ctx* c, char* host_dst, const void* dev_src, size_t byte
     return CM_OK;
 }
 
-// Issue the pending tap drain: one copy-engine D2H of the run's contiguous source range into
-// the ring, then one launch that publishes the run's tap flags.  Small shards (Llama's
-// norm buckets, the one-shot path) would otherwise cost 4 API calls each on the host.
+// Issue the pending tap drain: one D2H of the run's contiguous source range into the ring.
+// The iteration's tap flags are published once, after its last drain (restore can only use
+// a slot whose every bucket is in, so per-bucket flags would buy nothing -- and a flag kernel
+// between two copies idles the copy engine while its launch is fetched over the busy link).
+// Small shards (Llama's norm buckets, the one-shot path) coalesce into one copy.
 static cm_status flush_drain(cm_ctx* c, cudaStream_t s) {
     if (c->dr_b0 < 0) return CM_OK;
     CU(cudaEventRecord(c->ev_ar, s));
@@ -1224,11 +1226,6 @@ static cm_status flush_drain(cm_ctx* c, cudaStream_t s) {
         cm_status st = d2h(c, c->dr_dst, c->dr_src, c->dr_bytes, c->cs_tap);
         if (st != CM_OK) return st;
     }
-    const int slot = (int)(c->dr_iter % c->D);
-    volatile uint64_t* fl = to_dev(c, slot_flags(c, slot) + c->dr_b0);
-    publish_range_kernel<<<1, 32, 0, c->cs_tap>>>(fl, c->dr_b1 - c->dr_b0 + 1, (uint64_t)(c->dr_iter + 1));
-    c->launches++;
-    CHECK_LAUNCH();
     c->dr_b0 = c->dr_b1 = -1;
     c->dr_bytes = 0;
     return CM_OK;
@@ -1420,6 +1417,12 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     if (c->issued_count == (int)c->buckets.size()) {
         cm_status st = flush_drain(c, s);
         if (st != CM_OK) return st;
+        if (!c->no_tap && (c->ce_tap || staged) && !c->ablate_no_drain) {
+            volatile uint64_t* fl = to_dev(c, slot_flags(c, slot));
+            publish_range_kernel<<<1, 256, 0, c->cs_tap>>>(fl, (int)c->buckets.size(), (uint64_t)(t + 1));
+            c->launches++;
+            CHECK_LAUNCH();
+        }
     }
     if (!c->no_tap && c->issued_count == (int)c->buckets.size()) {
         const bool via_ce = c->ce_tap || staged;
