@@ -164,17 +164,22 @@ def host_link_peaks(dev):
     d = torch.empty(n, dtype=torch.uint8, device=dev)
     h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     out = {}
+    reps = 10
     for name, fn in (("d2h", lambda: h.copy_(d, non_blocking=True)), ("h2d", lambda: d.copy_(h, non_blocking=True))):
         for _ in range(2):
             fn()
         torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        for _ in range(5):
+        for _ in range(reps):
             fn()
         b.record()
         torch.cuda.synchronize()
-        out[name] = 5 * n / (a.elapsed_time(b) * 1e-3) / 1e9
+        # every rank moved reps * n bytes; the slowest rank's time is the concurrent rate
+        ms = max_over_ranks(a.elapsed_time(b)) if dist.is_initialized() else a.elapsed_time(b)
+        out[name] = reps * n / (ms * 1e-3) / 1e9
     # the same D2H into memory like the shadow segment's (a shared mmap registered with
     # cudaHostRegister, 4 KiB pages) -- what the tap drains and persists actually write to
     try:

@@ -167,6 +167,7 @@ struct cm_ctx {
     bool ablate_no_drain = false;         // ablation only: staged taps never reach the host ring
     bool lazy_exit = true;                // all-reduce kernels without exit barrier; the training
                                           // step's entry barrier fences the iteration instead
+    int64_t drain_flush = 8ll << 20;      // a pending drain run is issued once it holds this much
     int drain_ctas = -1;                  // D2H of tap drains / persists: 0 copy engine, k>0 k-CTA SM
                                           // drain, -1 auto (SM drain when the link demand is low)
     double iter_period_s = 0.0;           // EMA of the host period between training steps
@@ -570,6 +571,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
     else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
+    else if (k == "drain_flush_bytes" && value >= 0 && value <= kDrainCoalesce) c->drain_flush = value;
     else if (k == "ar_impl" && (value == 0 || value == 1)) c->ar_impl = (int)value;
     else if (k == "ar_pipe_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_pipe_blocks = (int)value;
     // cost decomposition only (tools/model_mode.py): the staged tap's copy-engine drain is not
@@ -1406,8 +1408,9 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         }
         c->dr_b1 = bucket;
         c->dr_bytes += bytes;
-        // a large run goes now; the iteration's last bucket flushes below
-        if (c->dr_bytes >= (size_t)kDrainCoalesce) {
+        // a run goes as soon as it is big enough to amortise a copy (small shards merge; the
+        // link must not idle behind a long run); the iteration's last bucket flushes below
+        if (c->dr_bytes >= (size_t)c->drain_flush) {
             cm_status st = flush_drain(c, s);
             if (st != CM_OK) return st;
         }
