@@ -314,7 +314,23 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *                         blocks of the n-rank instance; must be equal on every rank)
  *   "ar_blocks_tap_only"  grid cap of the all-reduce kernel at n == 1, where it is only the
  *                         PCIe-bound tap (default 32: leaves SMs to the shadow and training)
- *   "shadow_blocks"       grid cap of the vectorised shadow AdamW                          */
+ *   "shadow_blocks"       grid cap of the vectorised shadow AdamW
+ * Collective knobs (every rank must set the same value, before the first all-reduce):
+ *   "oneshot_max_bytes"   buckets up to this size take the one-shot push kernel (SURVEY 8
+ *                         f2; default 2 MiB / n, at most 1 MiB; 0 disables)
+ *   "lazy_exit"           1 (default): no exit barrier per bucket, the training step's
+ *                         optimizer kernel starts with one iteration fence; 0: an exit
+ *                         barrier per bucket (each all-reduce a complete collective)
+ *   "ar_impl"             0 (default) unrolled two-shot kernel, 1 software-pipelined variant
+ *   "ar_pipe_blocks"      grid of ar_impl 1 (default 148, one block per SM)
+ * Per-rank knobs:
+ *   "drain_ctas"          how tap drains and snapshot persists reach the host: -1 (default)
+ *                         auto policy from the measured step period, 0 copy
+ *                         engine, k > 0 a k-CTA SM drain kernel
+ *   "drain_flush_bytes"   a pending run of adjacent tap drains is issued at this size
+ *                         (default 8 MiB, at most 64 MiB)
+ *   "ablate_no_drain"     1: staged taps are never drained to the host ring (cost ablation;
+ *                         only with CM_FLAG_NO_SHADOW -- restore would be impossible)        */
 cm_status cm_set_param(cm_ctx *ctx, const char *key, int64_t value);
 
 /* cm_timing -- per-kernel device timing with CUDA events recorded on each kernel's own
