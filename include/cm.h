@@ -287,6 +287,8 @@ typedef struct {
     int32_t drain_ctas;                 /* how tap drains / snapshot persists reach the host
                                            now: 0 copy engine, k > 0 a k-CTA SM drain kernel
                                            (cm_set_param "drain_ctas": -1 auto, the default) */
+    int32_t numa_node;                  /* NUMA node the host segment was placed on, -1 none
+                                           (cm_set_param "numa_node")                     */
     int64_t padded_numel, shard_numel;  /* P_pad; sum over buckets of E_b/n               */
     int64_t shadow_step;                /* last step the shadow published                 */
     int64_t launches;                   /* kernels this context launched so far           */
@@ -323,10 +325,16 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *                         barrier per bucket (each all-reduce a complete collective)
  *   "ar_impl"             0 (default) unrolled two-shot kernel, 1 software-pipelined variant
  *   "ar_pipe_blocks"      grid of ar_impl 1 (default 148, one block per SM)
+ *   "zero1_impl"          ZeRO-1 AdamW + parameter all-gather kernel: 1 (default) two
+ *                         4-element groups per thread in flight, 0 one (ablation)
  * Per-rank knobs:
  *   "drain_ctas"          how tap drains and snapshot persists reach the host: -1 (default)
  *                         auto policy from the measured step period, 0 copy
  *                         engine, k > 0 a k-CTA SM drain kernel
+ *   "numa_node"           NUMA placement of the host shadow segment (set before cm_connect):
+ *                         -2 (default) the node of the GPU's PCIe root from sysfs, -1 the
+ *                         kernel's first-touch default, k >= 0 node k; MPOL_PREFERRED, best
+ *                         effort (cm_info.numa_node reports the outcome)
  *   "drain_flush_bytes"   a pending run of adjacent tap drains is issued at this size
  *                         (default 8 MiB, at most 64 MiB)
  *   "ablate_no_drain"     1: staged taps are never drained to the host ring (cost ablation;

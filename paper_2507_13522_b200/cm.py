@@ -55,7 +55,7 @@ class cm_sgd(C.Structure):
 class cm_info(C.Structure):
     _fields_ = [("n_buckets", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
                 ("ring_depth", C.c_int32), ("grad_dtype", C.c_int32), ("shadow_place", C.c_int32),
-                ("peers_in_process", C.c_int32), ("drain_ctas", C.c_int32), ("padded_numel", C.c_int64),
+                ("peers_in_process", C.c_int32), ("drain_ctas", C.c_int32), ("numa_node", C.c_int32), ("padded_numel", C.c_int64),
                 ("shard_numel", C.c_int64), ("shadow_step", C.c_int64), ("launches", C.c_int64),
                 ("layout_hash", C.c_uint64)]
 

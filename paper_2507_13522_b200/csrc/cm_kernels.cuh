@@ -582,7 +582,10 @@ __device__ __forceinline__ void wt_compute_store(const AdamParams& P, int64_t e,
     if constexpr (OPT == kOptAdamW) __stcs(reinterpret_cast<float4*>(P.v_out + e), v);
 }
 
-template <typename G, int OPT>
+// PAIR: two tiles per iteration (16 loads in flight per thread, ~100 registers, 2 blocks of
+// 256 per SM); !PAIR: one tile per iteration (8 loads, <= 64 registers, 4 blocks per SM:
+// twice the warps to overlap one warp's IEEE div/sqrt chain with other warps' loads)
+template <typename G, int OPT, bool PAIR = true>
 __device__ __forceinline__ void wt_body(const AdamParams& P) {
     if (P.fence_n) block_barrier(P.pads, P.fence_n, P.fence_rank, P.epoch, 0);
     const int lane = threadIdx.x & 31;
@@ -590,7 +593,7 @@ __device__ __forceinline__ void wt_body(const AdamParams& P) {
     const int64_t nwarps = ((int64_t)gridDim.x * kAdamThreads) >> 5;
     const int64_t tiles = P.n / kWarpTile;
     int64_t t = warp;
-    for (; t + nwarps < tiles; t += 2 * nwarps) {
+    for (; PAIR && t + nwarps < tiles; t += 2 * nwarps) {
         const int64_t a0 = t * kWarpTile + 4 * lane, a1 = a0 + 128;
         const int64_t b0 = (t + nwarps) * kWarpTile + 4 * lane, b1 = b0 + 128;
         float4 g[4], p[4], m[4], v[4] = {};
@@ -626,6 +629,12 @@ __device__ __forceinline__ void wt_body(const AdamParams& P) {
 template <typename G>
 __global__ void __launch_bounds__(kAdamThreads) adamw_wt_kernel(const AdamParams P) {
     wt_body<G, kOptAdamW>(P);
+}
+
+// one tile per iteration, 4 blocks per SM (cm_set_param("adamw_impl", 3))
+template <typename G>
+__global__ void __launch_bounds__(kAdamThreads, 4) adamw_wt1_kernel(const AdamParams P) {
+    wt_body<G, kOptAdamW, false>(P);
 }
 
 // SGD-momentum over the same warp tiles: HBM sizeof(G) + 8 read + 8 write B/elem
@@ -787,45 +796,77 @@ struct Zero1Params {
     float rec[10];
     int32_t rec_kind;
     int64_t step;
+    int unroll2;                    // 1: two groups per thread in flight (default), 0: one
 };
 
+// shard-local index j -> flat index of rank P.rank's element (b: running bucket index, j
+// non-decreasing per thread)
+__device__ __forceinline__ int64_t z1_flat(const Zero1Params& P, int64_t j, int& b) {
+    while (b + 1 < P.nb && j >= P.buckets[b + 1].shard_off) ++b;
+    const BucketDev& B = P.buckets[b];
+    return B.off + (int64_t)P.rank * (B.padded / P.n) + (j - B.shard_off);
+}
+template <typename G, int OPT>
+__device__ __forceinline__ void z1_load(const Zero1Params& P, int64_t j, int64_t flat, float4& g, float4& p,
+                                        float4& m, float4& v) {
+    if constexpr (std::is_same<G, F32Tag>::value) {
+        g = __ldcs(reinterpret_cast<const float4*>((const float*)P.g + j));
+    } else {
+        const uint2 w = __ldcs(reinterpret_cast<const uint2*>((const uint16_t*)P.g + j));
+        g = make_float4(bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y));
+    }
+    p = __ldcs(reinterpret_cast<const float4*>(P.p[P.rank] + flat));
+    m = __ldcs(reinterpret_cast<const float4*>(P.m + j));
+    if constexpr (OPT == kOptAdamW) v = __ldcs(reinterpret_cast<const float4*>(P.v + j));
+}
+template <int N, int OPT>
+__device__ __forceinline__ void z1_compute_store(const Zero1Params& P, int64_t j, int64_t flat, const float4& g,
+                                                 float4 p, float4 m, float4 v) {
+    if constexpr (OPT == kOptAdamW) {
+        adamw_elem(g.x, P.s, p.x, m.x, v.x);
+        adamw_elem(g.y, P.s, p.y, m.y, v.y);
+        adamw_elem(g.z, P.s, p.z, m.z, v.z);
+        adamw_elem(g.w, P.s, p.w, m.w, v.w);
+        __stcs(reinterpret_cast<float4*>(P.v + j), v);
+    } else {
+        sgd_elem(g.x, P.q, p.x, m.x);
+        sgd_elem(g.y, P.q, p.y, m.y);
+        sgd_elem(g.z, P.q, p.z, m.z);
+        sgd_elem(g.w, P.q, p.w, m.w);
+    }
+    __stcs(reinterpret_cast<float4*>(P.m + j), m);
+    const uint4 pw = make_uint4(__float_as_uint(p.x), __float_as_uint(p.y), __float_as_uint(p.z),
+                                __float_as_uint(p.w));
+#pragma unroll
+    for (int k = 0; k < N; ++k) st_v4(P.p[k] + flat, pw);   // own p + all-gather
+}
+
+// Grid-stride over 4-element groups of the shard; two groups per thread in flight (their
+// loads issued before either is reduced and stored): the kernel's NVLink egress is n-1
+// stores per group, and one group of loads per thread left the link under-fed.
 template <typename G, int N, int OPT = kOptAdamW>
 __global__ void __launch_bounds__(256) adamw_zero1_kernel(const Zero1Params P) {
     int b = 0;
     const int64_t groups = P.L / 4;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < groups;
-         q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (P.unroll2) {
+        for (; q + stride < groups; q += 2 * stride) {
+            const int64_t j0 = q * 4, j1 = (q + stride) * 4;
+            const int64_t f0 = z1_flat(P, j0, b), f1 = z1_flat(P, j1, b);
+            float4 g0, p0, m0, v0 = {}, g1, p1, m1, v1 = {};
+            z1_load<G, OPT>(P, j0, f0, g0, p0, m0, v0);
+            z1_load<G, OPT>(P, j1, f1, g1, p1, m1, v1);
+            z1_compute_store<N, OPT>(P, j0, f0, g0, p0, m0, v0);
+            z1_compute_store<N, OPT>(P, j1, f1, g1, p1, m1, v1);
+        }
+    }
+    for (; q < groups; q += stride) {
         const int64_t j = q * 4;
-        while (b + 1 < P.nb && j >= P.buckets[b + 1].shard_off) ++b;
-        const BucketDev B = P.buckets[b];
-        const int64_t flat = B.off + (int64_t)P.rank * (B.padded / P.n) + (j - B.shard_off);
-        float4 g;
-        if constexpr (std::is_same<G, F32Tag>::value) {
-            g = __ldcs(reinterpret_cast<const float4*>((const float*)P.g + j));
-        } else {
-            const uint2 w = __ldcs(reinterpret_cast<const uint2*>((const uint16_t*)P.g + j));
-            g = make_float4(bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y));
-        }
-        float4 p = __ldcs(reinterpret_cast<const float4*>(P.p[P.rank] + flat));
-        float4 m = __ldcs(reinterpret_cast<const float4*>(P.m + j));
-        if constexpr (OPT == kOptAdamW) {
-            float4 v = __ldcs(reinterpret_cast<const float4*>(P.v + j));
-            adamw_elem(g.x, P.s, p.x, m.x, v.x);
-            adamw_elem(g.y, P.s, p.y, m.y, v.y);
-            adamw_elem(g.z, P.s, p.z, m.z, v.z);
-            adamw_elem(g.w, P.s, p.w, m.w, v.w);
-            __stcs(reinterpret_cast<float4*>(P.v + j), v);
-        } else {
-            sgd_elem(g.x, P.q, p.x, m.x);
-            sgd_elem(g.y, P.q, p.y, m.y);
-            sgd_elem(g.z, P.q, p.z, m.z);
-            sgd_elem(g.w, P.q, p.w, m.w);
-        }
-        __stcs(reinterpret_cast<float4*>(P.m + j), m);
-        const uint4 pw = make_uint4(__float_as_uint(p.x), __float_as_uint(p.y), __float_as_uint(p.z),
-                                    __float_as_uint(p.w));
-#pragma unroll
-        for (int k = 0; k < N; ++k) st_v4(P.p[k] + flat, pw);   // own p + all-gather
+        const int64_t f = z1_flat(P, j, b);
+        float4 g, p, m, v = {};
+        z1_load<G, OPT>(P, j, f, g, p, m, v);
+        z1_compute_store<N, OPT>(P, j, f, g, p, m, v);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) write_record(P);
     if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 1);   // every shard landed everywhere

@@ -17,6 +17,7 @@
 #include <sys/socket.h>
 #include <sys/un.h>
 #include <sys/stat.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -170,6 +171,9 @@ struct cm_ctx {
     int64_t drain_flush = 8ll << 20;      // a pending drain run is issued once it holds this much
     int drain_ctas = -1;                  // D2H of tap drains / persists: 0 copy engine, k>0 k-CTA SM
                                           // drain, -1 auto (SM drain when the link demand is low)
+    int numa_req = -2;                    // host segment placement: -2 the GPU's NUMA node (auto),
+                                          // -1 kernel default (first touch), k >= 0 node k
+    int numa_used = -1;                   // node the segment was bound to (-1: none)
     double iter_period_s = 0.0;           // EMA of the host period between training steps
     std::chrono::steady_clock::time_point last_step_time{};
     char* peer_grad[kMaxRanks] = {};
@@ -189,9 +193,11 @@ struct cm_ctx {
     int ar_blocks_tap_only = 32;   // n == 1: the kernel is only the PCIe tap; leave SMs free
     int adamw_impl = 2;            // 0 vectorised, 1 TMA bulk-copy staged, 2 warp-tiled (measured best)
     int ar_impl = 0;               // 0 unrolled two-shot, 1 software-pipelined (one block per SM)
+    int zero1_impl = 1;            // ZeRO-1 AdamW + AG: 1 two groups per thread in flight, 0 one
     int ar_pipe_blocks = 148;
     int tma_blocks = 148;
     int wt_blocks = 296;
+    int wt1_blocks = 592;
 
     // shadow segment
     int shm_fd = -1;
@@ -441,6 +447,12 @@ static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaSt
             adamw_tma_kernel<F32Tag><<<grid, kTmaThreads, kTmaStages * TmaTile<F32Tag>::kStageBytes, s>>>(P);
         else
             adamw_tma_kernel<BF16Tag><<<grid, kTmaThreads, kTmaStages * TmaTile<BF16Tag>::kStageBytes, s>>>(P);
+    } else if (c->adamw_impl == 3) {
+        const int64_t tiles = P.n / kWarpTile;
+        const int64_t want = std::max<int64_t>(1, (tiles + kAdamThreads / 32 - 1) / (kAdamThreads / 32));
+        const int grid = (int)std::min<int64_t>(want, c->wt1_blocks);
+        if (c->dtype == CM_F32) adamw_wt1_kernel<F32Tag><<<grid, kAdamThreads, 0, s>>>(P);
+        else adamw_wt1_kernel<BF16Tag><<<grid, kAdamThreads, 0, s>>>(P);
     } else if (c->adamw_impl == 2 || P.fence_n) {
         const int64_t tiles = P.n / kWarpTile;
         const int64_t want = std::max<int64_t>(1, (tiles + kAdamThreads / 32 - 1) / (kAdamThreads / 32));
@@ -562,7 +574,7 @@ cm_status cm_join(cm_ctx* c, void* stream) {
 cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     if (!c || !key) return CM_ERR_ARG;
     const std::string k = key;
-    if (k == "adamw_impl" && value >= 0 && value <= 2) c->adamw_impl = (int)value;
+    if (k == "adamw_impl" && value >= 0 && value <= 3) c->adamw_impl = (int)value;
     else if (k == "adam_blocks" && value >= 1 && value <= 65535) c->adam_blocks = (int)value;
     else if (k == "ar_blocks_tap_only" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_tap_only = (int)value;
     else if (k == "shadow_blocks" && value >= 1 && value <= 65535) c->shadow_blocks = (int)value;
@@ -571,8 +583,10 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
     else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
+    else if (k == "numa_node" && value >= -2 && value < 64 && !c->seg) c->numa_req = (int)value;
     else if (k == "drain_flush_bytes" && value >= 0 && value <= kDrainCoalesce) c->drain_flush = value;
     else if (k == "ar_impl" && (value == 0 || value == 1)) c->ar_impl = (int)value;
+    else if (k == "zero1_impl" && (value == 0 || value == 1)) c->zero1_impl = (int)value;
     else if (k == "ar_pipe_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_pipe_blocks = (int)value;
     // cost decomposition only (tools/model_mode.py): the staged tap's copy-engine drain is not
     // issued, so the ring is never written -- restore and the host-ring fallback are invalid
@@ -738,6 +752,9 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
     int wocc = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wocc, adamw_wt_kernel<F32Tag>, kAdamThreads, 0);
     c->wt_blocks = c->sms * std::max(wocc, 1);
+    int wocc1 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wocc1, adamw_wt1_kernel<F32Tag>, kAdamThreads, 0);
+    c->wt1_blocks = c->sms * std::max(wocc1, 1);
     CU(cudaFuncSetAttribute(adamw_tma_kernel<F32Tag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kTmaStages * TmaTile<F32Tag>::kStageBytes));
     CU(cudaFuncSetAttribute(adamw_tma_kernel<BF16Tag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1088,6 +1105,35 @@ static cm_status snapshot_state(cm_ctx* c, int half, cudaStream_t s) {
     return CM_OK;
 }
 
+// NUMA node of the GPU's PCIe root (sysfs), -1 if unknown or a single-node host.
+static int gpu_numa_node(int dev) {
+    char bus[64];
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) return -1;
+    for (char* q = bus; *q; ++q) *q = (char)tolower((unsigned char)*q);
+    char path[160];
+    snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bus);
+    FILE* f = fopen(path, "r");
+    if (!f) return -1;
+    int node = -1;
+    if (fscanf(f, "%d", &node) != 1) node = -1;
+    fclose(f);
+    return node;
+}
+
+// Place the (not yet touched) host segment on one NUMA node, MPOL_PREFERRED: the tap drains
+// and snapshot persists are DMA writes from the GPU, and on a two-socket host pages that
+// first-touch put on the far socket cross the inter-socket link (tools/numa_probe.py).
+// Preferred, not bound: a node short of memory falls back instead of failing.  Best effort.
+static void bind_segment_numa(cm_ctx* c) {
+    c->numa_used = -1;
+    const int node = c->numa_req == -2 ? gpu_numa_node(c->dev) : c->numa_req;
+    if (node < 0 || node >= 64) return;
+    unsigned long mask = 1ul << node;
+    const long MPOL_PREFERRED_ = 1;
+    if (syscall(SYS_mbind, c->seg, c->seg_size, MPOL_PREFERRED_, &mask, 8 * sizeof mask + 1, 0) == 0)
+        c->numa_used = node;
+}
+
 static cm_status create_or_attach_segment(cm_ctx* c) {
     char name[256];
     snprintf(name, sizeof name, "/%s.r%d", c->shm_name.c_str(), c->rank);
@@ -1131,6 +1177,7 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
     if (mp == MAP_FAILED) return fail(c, CM_ERR_CONFIG, "mmap(%s) failed: %s", name, strerror(errno));
     c->seg = (char*)mp;
     c->hdr = (SegHeader*)c->seg;
+    if (!c->attach) bind_segment_numa(c);   // before the first touch (header write, pinning)
     if (c->attach) {
         const SegHeader& e = *c->hdr;
         if (e.magic != kMagic || e.version != kVersion || e.layout_hash != c->layout_hash ||
@@ -1515,6 +1562,7 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
         Z.pads = c->pads;
         Z.epoch = ++c->epoch;
         Z.hp_rec = P.hp_rec; Z.hp_kind = P.hp_kind; Z.hp_tag = P.hp_tag; Z.step = step;
+        Z.unroll2 = c->zero1_impl;
         memcpy(Z.rec, P.rec, sizeof Z.rec);
         Z.rec_kind = P.rec_kind;
         const int64_t want = (Z.L / 4 + 255) / 256;
@@ -1938,6 +1986,7 @@ cm_status cm_get_info(const cm_ctx* c, cm_info* o) {
     o->shadow_place = c->shadow_place;
     o->peers_in_process = c->in_process ? 1 : 0;
     o->drain_ctas = drain_ctas_now(c);
+    o->numa_node = c->numa_used;
     o->padded_numel = c->P_pad;
     o->shard_numel = c->shard_numel;
     o->shadow_step = c->hdr ? c->hdr->shadow_step : -1;

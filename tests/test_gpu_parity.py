@@ -352,10 +352,11 @@ def test_llama_shaped_bf16_sampled():
         close(g)
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2])
+@pytest.mark.parametrize("impl", [0, 1, 2, 3])
 @pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
 def test_adamw_implementations_bit_exact(impl, dtype):
-    """Every AdamW data-movement variant (vectorised, TMA-staged, warp-tiled) computes the
+    """Every AdamW data-movement variant (vectorised, TMA-staged, warp-tiled pair, warp-tiled
+    single tile) computes the
     same bits: the arithmetic is one device function; only the loads/stores differ."""
     numel = TABLES["mixed"]
     g = make_group(numel, 2, dtype)
@@ -501,14 +502,18 @@ def _zero1_shard_of(flat, plan, rank):
     return np.concatenate(out)
 
 
+@pytest.mark.parametrize("zimpl", [1, 0])
 @pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
-def test_zero1_bit_exact(n, dtype):
+def test_zero1_bit_exact(n, dtype, zimpl):
     """ZeRO-1 (f3): reduce-scatter + tap, AdamW on the own shard, fused parameter
     all-gather.  Every rank's full p, its shard-local m/v and the shadow equal the oracle
-    (the unsharded definition) bit for bit."""
+    (the unsharded definition) bit for bit, with two groups per thread in flight (default)
+    and with one (ablation)."""
     numel = TABLES["mixed"]
     g = make_group(numel, n, dtype, flags=cm.CM_FLAG_ZERO1)
+    for r in g.ranks:
+        r.ctx.set_param("zero1_impl", zimpl)
     plan, ref = oracle_for(numel, n, dtype, 1 << 20)
     try:
         assert g.ranks[0].m.numel() == plan.total // n

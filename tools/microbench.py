@@ -180,7 +180,8 @@ def shadow(place):
 
 
 TESTS = {"pcie": pcie, "adamw": adamw, "adamw_vec": lambda: adamw(0), "adamw_wt": lambda: adamw(2), "adamw_bf16": adamw_bf16,
-         "adamw_bf16_vec": lambda: adamw_bf16(0), "adamw_bf16_wt": lambda: adamw_bf16(2), "gen": gen, "tap": tap,
+         "adamw_bf16_vec": lambda: adamw_bf16(0), "adamw_bf16_wt": lambda: adamw_bf16(2),
+         "adamw_wt1": lambda: adamw(3), "adamw_bf16_wt1": lambda: adamw_bf16(3), "gen": gen, "tap": tap,
          "tap16": lambda: tap(blocks=16), "tap64": lambda: tap(blocks=64), "tap148": lambda: tap(blocks=148),
          "tap_ce": lambda: tap(cm.CM_FLAG_TAP_COPYENGINE, "tap via copy engine (ablation)"),
          "tap_staged": lambda: tap(0, "staged tap (kernel -> HBM staging, copy-engine drain)"),
