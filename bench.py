@@ -449,7 +449,13 @@ def isolated_kernels(args, dtype, cap, numel):
 
 def run_e2e(args, R, S_bytes, es):
     """Per step: H2D copy of this step's gradients from pinned host memory, the hot path,
-    and a D2H read of the step's result (the shadow's published step, 8 bytes)."""
+    and a D2H read of the step's result (the shadow's published step, 8 bytes).
+
+    The inputs are double-buffered like a data loader's prefetch: step t+1's gradients are
+    copied (copy stream) into an HBM landing buffer while step t runs, and moved into the
+    registered grad buffer (one HBM copy) when step t+1 starts.  Every timed step's H2D is
+    issued inside the timed region (the first one is not prefetched; the last step
+    prefetches nothing), so the region holds exactly one input copy per step."""
     import torch
     from paper_2507_13522_b200 import cm
     grad = R.r.grad
@@ -458,13 +464,33 @@ def run_e2e(args, R, S_bytes, es):
         R.r.ctx.gen_grads(R.seed, 10_000 + i, R.gscale, R.stream)
         R.stream.synchronize()
         host[i].copy_(grad)
+    land = torch.empty_like(grad)
+    cs = torch.cuda.Stream(grad.device)
+    free = torch.cuda.Event()
+    free.record(R.stream)
     out = torch.empty(1, dtype=torch.int64, pin_memory=True)
     dev_flag = torch.empty(1, dtype=torch.int64, device=grad.device)
     c = R.r.ctx
+    st = {"i": 0, "k": 0, "ready": None}
+
+    def h2d(t):
+        cs.wait_event(free)                                   # the landing buffer was consumed
+        with torch.cuda.stream(cs):
+            land.copy_(host[t & 1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        st["ready"] = ev
 
     def step():
+        if st["ready"] is None:
+            h2d(R.t)
+        R.stream.wait_event(st["ready"])
         with torch.cuda.stream(R.stream):
-            grad.copy_(host[R.t & 1], non_blocking=True)
+            grad.copy_(land, non_blocking=True)
+        free.record(R.stream)
+        st["ready"] = None
+        if st["i"] + 1 < st["k"]:
+            h2d(R.t + 1)                                      # prefetch: overlaps this step
         for b in range(R.n_buckets):
             c.allreduce_multicast(b, R.t, R.stream)
         c.apply_step(R.t + 1, stream=R.stream, **R.hp)
@@ -473,16 +499,21 @@ def run_e2e(args, R, S_bytes, es):
             dev_flag.fill_(R.t + 1)
             out.copy_(dev_flag, non_blocking=True)
         R.t += 1
+        st["i"] += 1
 
-    for _ in range(max(2, args.warmup // 2)):
-        step()
+    def run(k):
+        st["i"], st["k"], st["ready"] = 0, k, None
+        return time_steps(step, [R.stream, R.side, cs], k, c)
+
+    run(max(2, args.warmup // 2))
     R.sync()
+    cs.synchronize()
     k = max(3, args.steps // 2)
-    ms = time_steps(step, [R.stream, R.side], k, c)
-    ms = max_over_ranks(ms)
+    ms = max_over_ranks(run(k))
     return {"value": 1000.0 / (ms / k) * R.n, "unit": UNIT, "h2d_bytes_per_step": S_bytes,
             "d2h_bytes_per_step": 8, "ms_per_step": ms / k,
-            "note": "pinned-host grads copied H2D each step inside the timed region; per rank"}
+            "note": "pinned-host grads copied H2D each step inside the timed region (step t+1's "
+                    "copy overlaps step t, HBM landing buffer); per rank"}
 
 
 def run_nccl_baseline(args, rank, world, local, numel, dtype, cap):

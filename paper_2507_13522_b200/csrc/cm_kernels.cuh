@@ -418,14 +418,31 @@ struct AdamScalars {
     float c1, c2, B1, B2, bc1, bc2, inv_n, lr, eps, wd;
 };
 
+// IEEE-exact x / y and sqrt(x) that keep a zero operand off the slow path: the compiled
+// __fdiv_rn / __fsqrt_rn check their operands (FCHK) and branch to a subroutine for zero
+// and denormal inputs, and one such lane stalls its whole warp.  Zero moments are common
+// (an element whose gradient has been exactly zero since the start: untouched embedding
+// rows, 1 in 256 bf16 generator values), so the zero case is answered directly:
+// +-0 / y = +-0 for y > 0 and sqrt(+-0) = +-0, both exactly what IEEE 754 returns.
+__device__ __forceinline__ float div_rn_z(float x, float y) {
+    const bool z = (x == 0.0f) && (y > 0.0f);
+    const float q = __fdiv_rn(z ? 1.0f : x, z ? 1.0f : y);
+    return z ? x : q;
+}
+__device__ __forceinline__ float sqrt_rn_z(float x) {
+    const bool z = (x == 0.0f);
+    const float r = __fsqrt_rn(z ? 1.0f : x);
+    return z ? x : r;
+}
+
 __device__ __forceinline__ void adamw_elem(float R, const AdamScalars& s, float& p, float& m, float& v) {
     const float g = __fmul_rn(R, s.inv_n);
     const float mm = __fadd_rn(__fmul_rn(s.B1, m), __fmul_rn(s.c1, g));
     const float vv = __fadd_rn(__fmul_rn(s.B2, v), __fmul_rn(s.c2, __fmul_rn(g, g)));
-    const float mh = __fdiv_rn(mm, s.bc1);
-    const float vh = __fdiv_rn(vv, s.bc2);
-    const float d = __fadd_rn(__fsqrt_rn(vh), s.eps);
-    const float upd = __fadd_rn(__fdiv_rn(mh, d), __fmul_rn(s.wd, p));
+    const float mh = div_rn_z(mm, s.bc1);
+    const float vh = div_rn_z(vv, s.bc2);
+    const float d = __fadd_rn(sqrt_rn_z(vh), s.eps);
+    const float upd = __fadd_rn(div_rn_z(mh, d), __fmul_rn(s.wd, p));
     p = __fsub_rn(p, __fmul_rn(s.lr, upd));
     m = mm;
     v = vv;

@@ -661,3 +661,48 @@ def test_pipelined_allreduce_kernel_bit_exact(n, dtype):
             np.testing.assert_array_equal(bits(ring_flat(g, t % 2)), bits(ref.T), err_msg=f"tap t {t}")
     finally:
         close(g)
+
+
+@pytest.mark.parametrize("impl", [2, 0, 1])
+@pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
+def test_adamw_zero_gradients_bit_exact(dtype, impl):
+    """Exact zeros through the AdamW divisions (the zero-operand fast path of div_rn_z /
+    sqrt_rn_z): elements whose gradient is +0 or -0 on every rank at every step (moments stay
+    0: 0/bc1, 0/bc2, sqrt(0), 0/eps), elements zero only at some steps, and the rest
+    generated.  Train, shadow and tap equal the oracle bit for bit."""
+    import torch
+    numel = TABLES["mixed"]
+    n = 2
+    g = make_group(numel, n, dtype)
+    for r in g.ranks:
+        r.ctx.set_param("adamw_impl", impl)
+    plan, ref = oracle_for(numel, n, dtype, 1 << 20)
+    idx = np.arange(plan.total)
+    always = idx % 3 == 0
+    neg = (idx % 6 == 3) & plan.used_mask()
+    try:
+        for t in range(4):
+            grads = [O.gen_grads(plan, 0, r, t, dtype, W.GRAD_SCALE).copy() for r in range(n)]
+            sometimes = (idx + t) % 5 == 0
+            for a in grads:
+                a[always | sometimes] = 0
+                a[neg & ~always] = 0x8000 if dtype == cm.CM_BF16 else np.float32(-0.0)
+            for r, a in zip(g.ranks, grads):
+                src = torch.from_numpy(a.view(np.int16) if dtype == cm.CM_BF16 else a)
+                if dtype == cm.CM_BF16:
+                    r.grad.view(torch.int16).copy_(src)
+                else:
+                    r.grad.copy_(src)
+            torch.cuda.synchronize()
+            g.step(gen=False)
+            ref.step(grads=grads)
+            g.sync()
+            for r in g.ranks:
+                np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p), err_msg=f"p t {t}")
+                np.testing.assert_array_equal(bits(t2np(r.m)), bits(ref.m), err_msg=f"m t {t}")
+                np.testing.assert_array_equal(bits(t2np(r.v)), bits(ref.v), err_msg=f"v t {t}")
+                assert r.ctx.verify(g.stream) == -1
+            np.testing.assert_array_equal(bits(ring_flat(g, t % 2)), bits(ref.T), err_msg=f"tap t {t}")
+        assert np.count_nonzero(bits(t2np(g.ranks[0].m))[always] != 0) == 0
+    finally:
+        close(g)
