@@ -109,45 +109,60 @@ def max_over_ranks(x: float) -> float:
 
 # ---------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region.
+
+    nvidia-smi is started (and its first row awaited) before the region opens, so even a
+    region of a few hundred ms holds samples; only rows read between the region's start and
+    its end (plus one sampling interval of read lag) are reported."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    INTERVAL_MS = 50
 
     def __init__(self, index):
         self.index, self.rows, self.proc = index, [], None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.INTERVAL_MS)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
+            deadline = time.monotonic() + 15.0
+            while not self.rows and time.monotonic() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.t0 = time.monotonic()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.monotonic(), [x.strip() for x in line.split(",")]))
 
     def __exit__(self, *a):
+        self.t1 = time.monotonic()
         if self.proc:
-            time.sleep(0.15)
+            deadline = self.t1 + 0.5
+            while time.monotonic() < deadline and not any(ts >= self.t1 for ts, _ in self.rows):
+                time.sleep(0.01)
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
     def summary(self):
-        if not self.rows:
+        lag = 2 * self.INTERVAL_MS / 1000.0
+        rows = [r for ts, r in self.rows if self.t0 is not None and self.t0 <= ts <= self.t1 + lag]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "region_s": round(self.t1 - self.t0, 3)}
 
 
 # ---------------------------------------------------------------------------- measurements
@@ -372,6 +387,19 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
                                    "persist to the host snapshot every K steps (copy engine)"}
     gen_ms = kms[3] / max(kcnt[3], 1)
     kern["gen_grads"] = {"avg_ms": gen_ms, "launches": kcnt[3], "share": kms[3] / ms}
+    # the host link's busy time: summed durations of the tap drain copies (one stream) and
+    # of the snapshot persist copies (another stream; the two can overlap), per step
+    if kcnt[5] or kcnt[6]:
+        tap_b = S_bytes / n
+        kern["host_link_busy"] = {
+            "tap_drain_ms_per_step": kms[5] / args.steps, "tap_drains_per_step": kcnt[5] / args.steps,
+            "tap_drain_GBps_while_busy": tap_b / (kms[5] / args.steps * 1e-3) / 1e9 if kms[5] else None,
+            "persist_ms_per_step": kms[6] / args.steps, "persists_per_step": kcnt[6] / args.steps,
+            "persist_GBps_while_busy": (sh_d2h * args.steps) / (kms[6] * 1e-3) / 1e9 if kms[6] else None,
+            "busy_frac_of_step": (kms[5] + kms[6]) / ms,
+            "what": "copy durations on the drain / persist streams (events around each copy, after its stream "
+                    "waits); busy_frac < 1 means the link idled part of the step, a low GB/s while busy means "
+                    "slow copies"}
     traf = traffic_table().get(f"{args.workload}_n{n}_{args.shadow}", {})
     for k in kern:
         if k in traf:
@@ -696,7 +724,15 @@ def main():
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res.get("e2e"),
             "gpu_launches": res["launches"], "clocks": res["clocks"],
             "nockpt_nccl": base, "nockpt_ours": ours_nockpt, "model_mode": model, "variants": variants,
-            "ckpt_overhead_pct_vs_nccl": overhead,
+            # the paper's claim is the model-mode number (a real fwd/bwd to hide under); the
+            # synthetic step has no compute, so its checkpoint is the host link's time alone
+            "ckpt_overhead_pct_vs_nccl": {
+                "model_mode": model["ckpt_overhead_pct_vs_nccl"] if model else None,
+                "synthetic_no_compute": overhead,
+                "note": "model_mode: GPT-2 fwd/bwd + per-iteration checkpoint vs torch DDP on NCCL (the "
+                        "paper's claim, target <= 2%); synthetic_no_compute: the timed step above (only the "
+                        "hot path, no model), where the tap + snapshot bytes over the host link are the "
+                        "whole step (roofline.bound = host_link)"},
             "shadow_bit_identical": res["shadow_bit_identical"], "kernels": res["kernels"],
             "host_issue_ms_per_step": res["host_issue_ms_per_step"],
             "ms_step_kernel_timing_pass": res["ms_step_kernel_timing_pass"],

@@ -258,9 +258,11 @@ class Context:
         self._check(lib().cm_set_param(self._ctx, key.encode(), int(value)))
 
     def timing(self, enable):
-        """enable=True starts per-kernel timing; enable=False returns (ms[5], counts[5])."""
-        ms = (C.c_double * 5)()
-        cnt = (C.c_int64 * 5)()
+        """enable=True starts per-kernel timing; enable=False returns (ms[7], counts[7]):
+        classes 0-4 kernels (all-reduce, AdamW, shadow AdamW, gen, restore copy), 5 tap
+        drains, 6 snapshot persists."""
+        ms = (C.c_double * 7)()
+        cnt = (C.c_int64 * 7)()
         self._check(lib().cm_timing(self._ctx, 1 if enable else 0, ms, cnt))
         return list(ms), list(cnt)
 

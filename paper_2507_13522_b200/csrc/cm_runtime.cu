@@ -538,6 +538,7 @@ static cudaEvent_t timing_event(cm_ctx* c) {
     }
     return c->ev_pool[c->ev_used++];
 }
+constexpr int kTimingClasses = 7;   // cm_timing: 5 kernel classes + tap drains + persists
 struct TimedScope {
     cm_ctx* c; int cls; cudaStream_t s; cudaEvent_t a = nullptr;
     TimedScope(cm_ctx* c_, int cls_, cudaStream_t s_) : c(c_), cls(cls_), s(s_) {
@@ -604,8 +605,8 @@ cm_status cm_timing(cm_ctx* c, int32_t enable, double* ms_out, int64_t* count_ou
         return CM_OK;
     }
     c->timing = false;
-    double ms[5] = {0, 0, 0, 0, 0};
-    int64_t cnt[5] = {0, 0, 0, 0, 0};
+    double ms[kTimingClasses] = {};
+    int64_t cnt[kTimingClasses] = {};
     for (auto& t : c->timed) {
         CU(cudaEventSynchronize(t.second.second));
         float x = 0;
@@ -1248,7 +1249,9 @@ static int drain_ctas_now(const cm_ctx* c) {
     return std::min(kSmDrainMaxCtas, std::max(1, (int)std::ceil(demand / kSmDrainPerCta)));
 }
 
-static cm_status d2h(cm_ctx* c, char* host_dst, const void* dev_src, size_t bytes, cudaStream_t s) {
+// cls: cm_timing class of the copy (5 tap drain, 6 snapshot persist)
+static cm_status d2h(cm_ctx* c, char* host_dst, const void* dev_src, size_t bytes, cudaStream_t s, int cls) {
+    TimedScope ts(c, cls, s);
     const int ctas = drain_ctas_now(c);
     if (ctas <= 0 || (bytes & 15) || ((uintptr_t)dev_src & 15) || ((uintptr_t)host_dst & 15)) {
         CU(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, s));
@@ -1272,7 +1275,7 @@ static cm_status flush_drain(cm_ctx* c, cudaStream_t s) {
     CU(cudaEventRecord(c->ev_ar, s));
     CU(cudaStreamWaitEvent(c->cs_tap, c->ev_ar, 0));
     {
-        cm_status st = d2h(c, c->dr_dst, c->dr_src, c->dr_bytes, c->cs_tap);
+        cm_status st = d2h(c, c->dr_dst, c->dr_src, c->dr_bytes, c->cs_tap, 5);
         if (st != CM_OK) return st;
     }
     c->dr_b0 = c->dr_b1 = -1;
@@ -1677,7 +1680,7 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
                 // SGD leaves v untouched (all zero in every half): p and the velocity only
                 for (int k = 0; k < (rec.kind == kOptSgd ? 2 : 3); ++k)
                 {
-                    cm_status pst = d2h(c, (char*)(c->sh[ph][k] + lo), c->sd[hout][k] + lo, (size_t)len * 4, c->cs_d2h);
+                    cm_status pst = d2h(c, (char*)(c->sh[ph][k] + lo), c->sd[hout][k] + lo, (size_t)len * 4, c->cs_d2h, 6);
                     if (pst != CM_OK) return pst;
                 }
             }
@@ -1919,6 +1922,18 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
                                cudaMemcpyHostToDevice, s));
         c->hh_step[0] = me.snap[0];
         c->hh_step[1] = me.snap[1];
+        // The roll-forward persists step I over the "older" half.  Never let that be the
+        // source snapshot: a kill during the persist would leave this shard only a half
+        // beyond I (this shard ran ahead of the consolidation point), and the next restore
+        // could not reach I.  A half beyond I is stale anyway (training recomputes it), so
+        // it is invalidated first and becomes the persist target; the source stays intact.
+        // (A half in (b, I] cannot exist: it would roll to I over a subset of the same ring
+        // slots, and pick() takes the newest such base.)
+        const int other = 1 - bi;
+        if (me.snap[other] > I) {
+            c->hdr->half_step[other] = -1;
+            c->hh_step[other] = -1;
+        }
     } else {
         // DEVICE placement: the HBM halves are the snapshots (half i holds step snap[i], i = step&1)
         for (int i = 0; i < 2; ++i)

@@ -1,0 +1,43 @@
+"""Host logic of bench.py that needs no GPU: the clock sampler reports only rows read
+inside the timed region, and a short region still gets samples because nvidia-smi is
+started (and its first row awaited) before the region opens."""
+import os
+import stat
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def _fake_smi(tmp_path, reason="Not Active", startup_s=0.4):
+    p = tmp_path / "nvidia-smi"
+    p.write_text("#!/bin/bash\n"
+                 f"sleep {startup_s}\n"
+                 f"while true; do echo \"0, 1965, 1965, {reason}, Not Active, Not Active, Not Active\"; sleep 0.05; done\n")
+    p.chmod(p.stat().st_mode | stat.S_IEXEC)
+    return str(tmp_path)
+
+
+def test_short_region_is_sampled(tmp_path, monkeypatch):
+    monkeypatch.setenv("PATH", _fake_smi(tmp_path) + os.pathsep + os.environ["PATH"])
+    with bench.ClockSampler(0) as c:
+        time.sleep(0.2)
+    s = c.summary()
+    assert s["samples"] >= 2 and s["sm_mhz"] == 1965.0 and s["reasons"] == []
+
+
+def test_throttle_reason_reported(tmp_path, monkeypatch):
+    monkeypatch.setenv("PATH", _fake_smi(tmp_path, reason="Active") + os.pathsep + os.environ["PATH"])
+    with bench.ClockSampler(0) as c:
+        time.sleep(0.15)
+    assert c.summary()["reasons"] == ["hw_slowdown"]
+
+
+def test_missing_nvidia_smi_is_unsampled(tmp_path, monkeypatch):
+    monkeypatch.setenv("PATH", str(tmp_path))
+    with bench.ClockSampler(0) as c:
+        time.sleep(0.01)
+    assert c.summary()["reasons"] == ["unsampled"]

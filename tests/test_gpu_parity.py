@@ -706,3 +706,68 @@ def test_adamw_zero_gradients_bit_exact(dtype, impl):
         assert np.count_nonzero(bits(t2np(g.ranks[0].m))[always] != 0) == 0
     finally:
         close(g)
+
+
+def test_restore_keeps_its_source_snapshot_when_a_shard_ran_ahead():
+    """A shard whose shadow ran past the consolidation point I (rank 0 persisted step 8,
+    rank 1 can only reach 6): restore rolls rank 0 forward from its step-4 snapshot and
+    persists step 6 into the half holding the stale step 8 -- never over the step-4 source,
+    so a kill during that persist still leaves a half from which I is reachable.  Both
+    shards end bit-exact at I and continue bit-exact."""
+    from tests.gpu_util import shard_slices
+    numel = TABLES["ragged"]
+    n, K, D = 2, 4, 8
+    name = _name()
+    g = harness.VirtualGroup(numel, n, 0, cm.CM_F32, 1 << 20, name, D, cm.CM_SHADOW_HOST, 0, 0,
+                             persist_every=K)
+    g._shm = name
+    plan, ref = oracle_for(numel, n, cm.CM_F32, 1 << 20)
+    r0, r1 = g.ranks
+    try:
+        for _ in range(4):                                   # both shards persist step 4
+            g.step()
+        for t in (4, 5):                                     # both train; only rank 0's shadow
+            g.gen(t)
+            g.allreduce(t)
+            g.apply(t + 1)
+            r0.ctx.shadow_apply(t + 1, g.side)
+        for t in (6, 7):                                     # rank 0 alone runs ahead to step 8
+            r0.ctx.gen_grads(g.seed, t, g.gscale, g.stream)
+            for b in range(g.n_buckets):
+                r0.ctx.allreduce_multicast(b, t, g.stream)
+            r0.ctx.apply_step(t + 1, stream=g.stream, **g.hp)
+            r0.ctx.shadow_apply(t + 1, g.side)
+        g.sync()
+        assert [r.ctx.info().shadow_step for r in g.ranks] == [8, 4]
+        for r in g.ranks:
+            r.p.fill_(float("nan")); r.m.fill_(float("nan")); r.v.fill_(float("nan"))
+        torch.cuda.synchronize()
+        steps = [r.ctx.restore(g.stream) for r in g.ranks]
+        g.sync()
+        assert steps == [6, 6], steps
+        for _ in range(4):
+            ref.step()
+        p4 = ref.p.copy()
+        for _ in range(2):
+            ref.step()
+        for r in g.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            np.testing.assert_array_equal(bits(t2np(r.m)), bits(ref.m))
+            np.testing.assert_array_equal(bits(t2np(r.v)), bits(ref.v))
+        # rank 0's step-4 snapshot (the restore's source) survived the step-6 persist
+        L = r0.ctx.info().shard_numel
+        want = np.zeros(L, np.float32)
+        for lo, hi, s in shard_slices(r0):
+            want[s:s + (hi - lo)] = p4[lo:hi]
+        halves = [host_array(r0.ctx.shadow_view(h)[0], L, np.float32) for h in (0, 1)]
+        assert any(np.array_equal(bits(hp), bits(want)) for hp in halves)
+        g.t = 6
+        for _ in range(3):
+            g.step()
+            ref.step()
+        g.sync()
+        for r in g.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            assert r.ctx.verify(g.stream) == -1
+    finally:
+        close(g)

@@ -3,8 +3,14 @@ processes exit, only the host shadow segments survive), relaunch, attach, restor
 shadow, continue 100 iterations, and compare sampled elements of every rank's state with
 the oracle's uninterrupted trajectories, bit for bit.
 
-  python -m torch.distributed.run --nproc-per-node N tools/restore_bench.py phase1 <name> [k]
+  python -m torch.distributed.run --nproc-per-node N tools/restore_bench.py phase1 <name> [k] [more] [point]
+  python -m torch.distributed.run --nproc-per-node N tools/restore_bench.py phase2kill <name> [k] [more] [delay_s]
   python -m torch.distributed.run --nproc-per-node N tools/restore_bench.py phase2 <name> [k] [more]
+Kill points of phase 1: "step" (after k whole iterations, their shadow
+and drain work still in flight), "after_ar" (k whole iterations, then iteration k's
+gradients and all-reduces + taps issued, the optimizer step never reached).  phase2kill
+attaches, starts cm_restore and SIGKILLs itself after delay_s (a kill mid-restore, possibly
+mid-persist of the rolled-forward snapshot); phase 2 must still restore.
 Rank 0 of phase 2 prints one JSON line (restore wall time, restored step, bit-exactness).
 """
 import json
@@ -27,16 +33,22 @@ def main():
     phase, name = sys.argv[1], sys.argv[2]
     k = int(sys.argv[3]) if len(sys.argv) > 3 else 7
     more = int(sys.argv[4]) if len(sys.argv) > 4 else 100
+    extra = sys.argv[5] if len(sys.argv) > 5 else None
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, n = dist.get_rank(), dist.get_world_size()
     numel = W.numels(W.gpt2_small())
-    flags = cm.CM_FLAG_ATTACH if phase == "phase2" else 0
+    flags = cm.CM_FLAG_ATTACH if phase in ("phase2", "phase2kill") else 0
     R = harness.DistRank(numel, cm.CM_F32, W.CAP_BYTES, name, 16, cm.CM_SHADOW_HOST, flags, persist_every=8)
     if phase == "phase1":
         for _ in range(k):
             R.step()
+        if extra == "after_ar":
+            c = R.r.ctx
+            c.gen_grads(R.seed, R.t, R.gscale, R.stream)
+            for b in range(R.n_buckets):
+                c.allreduce_multicast(b, R.t, R.stream)
         # die with work still in flight (no stream sync, no finalize): whatever the GPUs did
         # not finish is lost; only the host shadow segments in /dev/shm survive
         dist.barrier()
@@ -47,6 +59,14 @@ def main():
     R.r.v.fill_(float("nan"))
     torch.cuda.synchronize()
     dist.barrier()
+    if phase == "phase2kill":
+        import signal
+        import threading
+        delay = float(extra) if extra else 0.02
+        threading.Timer(delay, lambda: os.kill(os.getpid(), signal.SIGKILL)).start()
+        R.r.ctx.restore(R.stream)
+        torch.cuda.synchronize()
+        time.sleep(10)                      # the timer fires (restore was faster than delay)
     t0 = time.perf_counter()
     I = R.r.ctx.restore(R.stream)
     torch.cuda.synchronize()
@@ -72,7 +92,8 @@ def main():
     ok_all = torch.tensor([float(same and ok_shadow)], dtype=torch.float64, device=R.r.p.device)
     dist.all_reduce(ok_all, op=dist.ReduceOp.MIN)
     if rank == 0:
-        print(json.dumps({"n": n, "killed_after_iterations": k, "restored_step": I, "restore_s_max_over_ranks": res[0].item(),
+        print(json.dumps({"n": n, "killed_after_iterations": k, "kill_point": os.environ.get("CM_KILL_POINT", "step"),
+                          "restored_step": I, "restore_s_max_over_ranks": res[0].item(),
                           "continued_iterations": more, "bit_exact_vs_oracle_and_shadow": bool(ok_all.item() == 1.0),
                           "sampled_elements_per_rank": int(len(idx)), "persist_every": 8, "ring_depth": 16}),
               flush=True)
