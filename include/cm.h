@@ -265,7 +265,9 @@ cm_status cm_shadow_apply(cm_ctx *ctx, int64_t step, void *side_stream);
  * tapped ring slots), rolls this rank's shard forward to I if needed, copies it host ->
  * device and all-gathers p/m/v to every rank over NVLink.  Blocks until done; returns I
  * in *restored_step; the caller resumes at iteration I.  CM_ERR_UNRECOVERABLE if no
- * common step exists.                                                                  */
+ * common step exists.  Host shadow: a rolled-forward step I is persisted into the half
+ * that is NOT the roll-forward source (a half beyond I is invalidated first), so a kill
+ * during restore leaves a segment from which the next cm_restore reaches I again.      */
 cm_status cm_restore(cm_ctx *ctx, int64_t *restored_step, void *stream);
 
 /* ------------------------------------------------------------------ inputs / checks

@@ -174,8 +174,11 @@ struct cm_ctx {
     int numa_req = -2;                    // host segment placement: -2 the GPU's NUMA node (auto),
                                           // -1 kernel default (first touch), k >= 0 node k
     int numa_used = -1;                   // node the segment was bound to (-1: none)
-    double iter_period_s = 0.0;           // EMA of the host period between training steps
-    std::chrono::steady_clock::time_point last_step_time{};
+    double iter_period_s = 0.0;           // EMA of the GPU's period between training steps
+    static constexpr int kStepEv = 8;     // events recorded after each step's optimizer kernel
+    cudaEvent_t ev_gstep[kStepEv] = {};
+    int64_t ev_gstep_step[kStepEv] = {-1, -1, -1, -1, -1, -1, -1, -1};
+    int64_t gper_last = 0;                // newest step whose period went into the estimate
     char* peer_grad[kMaxRanks] = {};
     float* peer_p[kMaxRanks] = {};
     float* peer_m[kMaxRanks] = {};
@@ -1236,6 +1239,10 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
 //   n > 1, demand  > 2.5 GB/s      -> 2 CTAs       (GPT-2 n=2: +1.6%, 1 CTA +3.3%;
 //                                                   Llama n=4: -1.3% vs NCCL, copy engine +0.3%)
 //   demand > 20 GB/s (nothing to hide under: the step is link-bound) -> copy engine
+// The step period is the GPU's (events after each step's optimizer kernel), not the host's:
+// the host runs ahead of the GPU, and a host-side period once mixed a sync before a timed
+// region into the estimate, sent the first iterations of a link-bound 2-GPU step to a 2-CTA
+// SM drain that cannot keep up, and made that step measure 8.2 or 12-14 ms by chance.
 constexpr double kSmDrainPerCta = 2.5e9;
 constexpr int kSmDrainMaxCtas = 2;
 constexpr double kLinkBoundDemand = 20e9;
@@ -1523,15 +1530,31 @@ cm_status cm_apply_step_sgd(cm_ctx* c, int64_t step, const cm_sgd* hp, void* str
     return apply_impl(c, step, r, stream);
 }
 
-static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* stream) {
-    {   // step period (host clock; the stream's backpressure ties it to the GPU's pace)
-        const auto now = std::chrono::steady_clock::now();
-        if (c->train_step > 0) {
-            const double dt = std::chrono::duration<double>(now - c->last_step_time).count();
-            c->iter_period_s = c->iter_period_s > 0.0 ? 0.8 * c->iter_period_s + 0.2 * dt : dt;
+// GPU period between consecutive training steps: the newest pair of step events (recorded
+// after each step's optimizer kernel on the training stream) that have both completed and
+// were not used yet.  Nothing completed yet (the host runs ahead): the estimate stands.
+// One long interval (a pause for evaluation, a sync) counts at most 4x the estimate.
+static void update_gpu_period(cm_ctx* c, int64_t step) {
+    constexpr int E = cm_ctx::kStepEv;
+    for (int64_t k = step - 1; k >= 2 && k > c->gper_last && k > step - E; --k) {
+        const int a = (int)((k - 1) % E), b = (int)(k % E);
+        if (c->ev_gstep_step[a] != k - 1 || c->ev_gstep_step[b] != k) continue;
+        if (cudaEventQuery(c->ev_gstep[b]) != cudaSuccess) continue;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c->ev_gstep[a], c->ev_gstep[b]) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
         }
-        c->last_step_time = now;
+        double dt = ms * 1e-3;
+        if (c->iter_period_s > 0.0) dt = std::min(dt, 4.0 * c->iter_period_s);
+        c->iter_period_s = c->iter_period_s > 0.0 ? 0.8 * c->iter_period_s + 0.2 * dt : dt;
+        c->gper_last = k;
+        return;
     }
+}
+
+static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* stream) {
+    update_gpu_period(c, step);
     const int slot = (int)((step - 1) % c->D);
     c->slot_sc[slot] = rec;
     c->slot_sc_step[slot] = step;
@@ -1588,6 +1611,12 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
         st = launch_adamw(c, P, c->adam_blocks, S(stream));
     }
     if (st != CM_OK) return st;
+    {   // the GPU step clock of the drain policy
+        const int k = (int)(step % cm_ctx::kStepEv);
+        if (!c->ev_gstep[k]) CU(cudaEventCreate(&c->ev_gstep[k]));
+        CU(cudaEventRecord(c->ev_gstep[k], S(stream)));
+        c->ev_gstep_step[k] = step;
+    }
     if (!c->no_tap && c->ce_tap)   // the caller may overwrite grads after this: taps first
         CU(cudaStreamWaitEvent(S(stream), c->ev_tap_done[slot], 0));
     c->train_step = step;
@@ -2192,6 +2221,7 @@ cm_status cm_finalize(cm_ctx* c) {
     if (c->d_done_ctr) cudaFree(c->d_done_ctr);
     if (c->d_bad) cudaFree(c->d_bad);
     for (auto e : c->ev_tap_done) cudaEventDestroy(e);
+    for (auto e : c->ev_gstep) if (e) cudaEventDestroy(e);
     for (auto e : c->ev_slot_free) cudaEventDestroy(e);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->cs_tap) cudaStreamDestroy(c->cs_tap);
