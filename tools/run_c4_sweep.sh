@@ -8,5 +8,5 @@ F=$OUT/${TAG}_sweep_n$N.jsonl; : > $F
 port=29950
 for T in ${TOKENS:-4096 8192 16384 32768}; do
   port=$((port + 1))
-  timeout 1200 $RUN --master-port $port tools/filler_mode.py --tokens $T --steps 4 --warmup 2 --ring-depth 8 --persist-every 8 >> $F 2>> $OUT/${TAG}_sweep_n$N.err
+  timeout 1200 $RUN --master-port $port tools/filler_mode.py --tokens $T --steps 3 --warmup 2 --ring-depth 8 --persist-every 8 >> $F 2>> $OUT/${TAG}_sweep_n$N.err
 done
