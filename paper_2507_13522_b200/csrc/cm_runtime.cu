@@ -1238,14 +1238,17 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
 //   n > 1, demand <= 2.5 GB/s      -> 1 CTA        (GPT-2 n=4: +0.9%; copy engine +3.3%)
 //   n > 1, demand  > 2.5 GB/s      -> 2 CTAs       (GPT-2 n=2: +1.6%, 1 CTA +3.3%;
 //                                                   Llama n=4: -1.3% vs NCCL, copy engine +0.3%)
-//   demand > 20 GB/s (nothing to hide under: the step is link-bound) -> copy engine
+//   demand > 12.5 GB/s (little to hide under: the step is near link-bound) -> copy engine
 // The step period is the GPU's (events after each step's optimizer kernel), not the host's:
 // the host runs ahead of the GPU, and a host-side period once mixed a sync before a timed
 // region into the estimate, sent the first iterations of a link-bound 2-GPU step to a 2-CTA
 // SM drain that cannot keep up, and made that step measure 8.2 or 12-14 ms by chance.
 constexpr double kSmDrainPerCta = 2.5e9;
 constexpr int kSmDrainMaxCtas = 2;
-constexpr double kLinkBoundDemand = 20e9;
+// Above ~half the 2-CTA SM drain's ~25 GB/s the SM drain queues up and stalls the step:
+// Llama-8B-shaped filler at n=4 (profiles/r01h_c4_sweep_n4.jsonl), T=8k tokens/GPU, 17 GB/s
+// of demand on 2 CTAs: +3.8% vs NCCL; T=16k, 10 GB/s on 2 CTAs: -1.35%.
+constexpr double kLinkBoundDemand = 12.5e9;
 static int drain_ctas_now(const cm_ctx* c) {
     if (c->drain_ctas >= 0) return c->drain_ctas;
     if (c->n == 1 || c->iter_period_s <= 0.0) return 0;
