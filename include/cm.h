@@ -331,7 +331,7 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *                         4-element groups per thread in flight, 0 one (ablation)
  * Per-rank knobs:
  *   "drain_ctas"          how tap drains and snapshot persists reach the host: -1 (default)
- *                         auto policy from the measured step period, 0 copy
+ *                         auto policy from the GPU-timed step period, 0 copy
  *                         engine, k > 0 a k-CTA SM drain kernel
  *   "numa_node"           NUMA placement of the host shadow segment (set before cm_connect):
  *                         -2 (default) the node of the GPU's PCIe root from sysfs, -1 the
