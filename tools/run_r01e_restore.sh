@@ -1,6 +1,8 @@
 #!/bin/bash
 # Restore source-snapshot fix: the new test passes with the fixed library and fails with the
-# library built before the fix (tools/exp/libcm_before_restore_fix.so), then the restore tests.
+# library built before the fix (tools/exp/libcm_before_restore_fix.so: nvcc of cm_runtime.cu at
+# commit dda0338^ -- i.e. before 4c5fc53 -- with build.py's flags; not kept in the tree), then
+# the restore tests.
 cd "$(dirname "$0")/.."
 OUT=gpurun_out; TAG=${1:-r01e_restore}
 K="source_snapshot"
