@@ -1,7 +1,7 @@
 #!/bin/bash
 # Restore source-snapshot fix: the new test passes with the fixed library and fails with the
-# library built before the fix (tools/exp/libcm_before_restore_fix.so: nvcc of cm_runtime.cu at
-# commit dda0338^ -- i.e. before 4c5fc53 -- with build.py's flags; not kept in the tree), then
+# library built before the fix (tools/exp/libcm_before_restore_fix.so: nvcc of cm_runtime.cu as
+# of 4c5fc53^, the parent of the fix commit, with build.py's flags; not kept in the tree), then
 # the restore tests.
 cd "$(dirname "$0")/.."
 OUT=gpurun_out; TAG=${1:-r01e_restore}
