@@ -44,7 +44,7 @@ class Rank:
         self.blob = self.ctx.register_buckets(self.numel, grad_dtype, cap_bytes, self.grad.data_ptr(),
                                               self.p.data_ptr(), self.m.data_ptr(), self.v.data_ptr())
         # A/B switches for tools (collective settings: every rank must use the same value)
-        for key in ("lazy_exit", "drain_ctas", "oneshot_max_bytes", "ar_impl", "ar_pipe_blocks", "drain_flush_bytes", "numa_node", "zero1_impl"):
+        for key in ("lazy_exit", "drain_ctas", "oneshot_max_bytes", "ar_impl", "ar_pipe_blocks", "drain_flush_bytes", "numa_node", "zero1_impl", "shadow_blocks"):
             val = os.environ.get("CM_" + key.upper())
             if val is not None:
                 self.ctx.set_param(key, int(val))
