@@ -15,6 +15,14 @@ Rank 0 prints ONE JSON line.  `value` is whole-job throughput: rank-iterations p
 (iterations/s x N; each rank-iteration reduces and checkpoints one local batch's
 gradients), max-over-ranks device time.  `--impl reference` times the CPU oracle (the
 tier's reference arm) on a bounded sample of the same workload.
+
+Beyond the base contract the line carries: `roofline` (the step's binding resource; the
+host link for the checkpointed synthetic step), `kernels` (per-kernel rooflines from live
+events, plus `host_link_busy`: the drain and persist copies' busy time and rates),
+`nockpt_ours` / `nockpt_nccl` (the same step without a checkpoint, on our kernels and on
+NCCL + torch fused AdamW), `model_mode` (GPT-2 fwd/bwd with per-iteration checkpoint vs
+torch DDP on NCCL -- the paper's claim), `ckpt_overhead_pct_vs_nccl` (model mode, and the
+synthetic step that has no compute to hide under), `cpu_baseline`, `e2e`, `clocks`.
 """
 from __future__ import annotations
 
