@@ -328,7 +328,9 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *   "ar_impl"             0 (default) unrolled two-shot kernel, 1 software-pipelined variant
  *   "ar_pipe_blocks"      grid of ar_impl 1 (default 148, one block per SM)
  *   "zero1_impl"          ZeRO-1 AdamW + parameter all-gather kernel: 1 (default) two
- *                         4-element groups per thread in flight, 0 one (ablation)
+ *                         4-element groups per thread in flight, 0 one (ablation), 2 the
+ *                         updated parameters staged in shared memory per 2048-element tile
+ *                         and pushed to every rank's p with cp.async.bulk stores
  * Per-rank knobs:
  *   "drain_ctas"          how tap drains and snapshot persists reach the host: -1 (default)
  *                         auto policy from the GPU-timed step period, 0 copy

@@ -889,6 +889,87 @@ __global__ void __launch_bounds__(256) adamw_zero1_kernel(const Zero1Params P) {
     if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 1);   // every shard landed everywhere
 }
 
+// ZeRO-1 with the parameter all-gather as bulk copies (cm_set_param("zero1_impl", 2)): the
+// updated parameters of a tile go into shared memory, and one elected thread pushes the
+// tile to its own p and to every peer's p with n cp.async.bulk stores (the bulk-copy engine
+// moves the bytes over NVLink; no per-thread remote stores).  Tiles never straddle a
+// bucket, so each tile is one contiguous range of every rank's flat p.  Two tile buffers:
+// a buffer is rewritten only after its previous bulk stores have read it.  Same element
+// arithmetic (adamw_elem / sgd_elem), same bits.
+constexpr int kZ1TmaThreads = 256;
+constexpr int kZ1TmaTile = 2048;   // elements: 8 KiB of fp32 parameters
+
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+template <typename G, int N, int OPT = kOptAdamW>
+__global__ void __launch_bounds__(kZ1TmaThreads) adamw_zero1_tma_kernel(const Zero1Params P) {
+    __shared__ __align__(128) float tile[2][kZ1TmaTile];
+    const bool leader = threadIdx.x == 0;
+    int b = 0;
+    int64_t base = 0;   // first tile index of bucket b
+    int buf = 0;
+    for (int64_t t = blockIdx.x;; t += gridDim.x) {
+        int64_t len = 0;
+        while (b < P.nb) {
+            len = P.buckets[b].padded / P.n;
+            const int64_t tb = (len + kZ1TmaTile - 1) / kZ1TmaTile;
+            if (t < base + tb) break;
+            base += tb;
+            ++b;
+        }
+        if (b >= P.nb) break;
+        const BucketDev& B = P.buckets[b];
+        const int64_t lo = (t - base) * kZ1TmaTile;
+        const int cnt = (int)min((int64_t)kZ1TmaTile, len - lo);          // a multiple of 4
+        const int64_t j0 = B.shard_off + lo;                                // shard-local
+        const int64_t f0 = B.off + (int64_t)P.rank * len + lo;              // flat
+        if (leader) bulk_wait_read1();   // the stores issued from this buffer two tiles ago
+        __syncthreads();
+        float4 g[2], p[2], m[2], v[2] = {};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int e = (u * kZ1TmaThreads + threadIdx.x) * 4;
+            if (e < cnt) z1_load<G, OPT>(P, j0 + e, f0 + e, g[u], p[u], m[u], v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int e = (u * kZ1TmaThreads + threadIdx.x) * 4;
+            if (e >= cnt) continue;
+            if constexpr (OPT == kOptAdamW) {
+                adamw_elem(g[u].x, P.s, p[u].x, m[u].x, v[u].x);
+                adamw_elem(g[u].y, P.s, p[u].y, m[u].y, v[u].y);
+                adamw_elem(g[u].z, P.s, p[u].z, m[u].z, v[u].z);
+                adamw_elem(g[u].w, P.s, p[u].w, m[u].w, v[u].w);
+                __stcs(reinterpret_cast<float4*>(P.v + j0 + e), v[u]);
+            } else {
+                sgd_elem(g[u].x, P.q, p[u].x, m[u].x);
+                sgd_elem(g[u].y, P.q, p[u].y, m[u].y);
+                sgd_elem(g[u].z, P.q, p[u].z, m[u].z);
+                sgd_elem(g[u].w, P.q, p[u].w, m[u].w);
+            }
+            __stcs(reinterpret_cast<float4*>(P.m + j0 + e), m[u]);
+            *reinterpret_cast<float4*>(&tile[buf][e]) = p[u];
+        }
+        fence_proxy_async_smem();        // this thread's smem writes -> visible to the bulk copies
+        __syncthreads();
+        if (leader) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) bulk_store(P.p[k] + f0, &tile[buf][0], (uint32_t)cnt * 4u);
+            bulk_commit();
+        }
+        buf ^= 1;
+    }
+    if (leader) {
+        bulk_wait0();                    // every bulk store of this block has completed
+        fence_proxy_async_global();      // ... and is ordered before the generic release below
+        __threadfence_system();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) write_record(P);
+    if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 1);   // every shard landed everywhere
+    else __syncthreads();
+}
+
 // ------------------------------------------------------------------ shard gather/scatter
 // Shard-local index j of rank r <-> flat index off_b + r*E_b/n + (j - shard_off_b).
 // dir 0 (snapshot): flat device p/m/v of this rank -> shard-local dst arrays.

@@ -133,6 +133,7 @@ struct cm_ctx {
     bool no_tap = false, attach = false, ce_tap = false, no_shadow = false, staged_tap = false;
     bool zero1 = false;                   // CM_FLAG_ZERO1: sharded optimizer state
     int zero1_blocks = 296;
+    int zero1_tma_blocks = 592;
     void* stage_buf[2] = {};              // default tap: HBM staging of the reduced shard
     cudaEvent_t ev_stage_free[2] = {};    // staging half drained to the host ring
     cudaEvent_t ev_ar_done[2] = {};       // all all-reduce kernels of the half's iteration done
@@ -196,7 +197,8 @@ struct cm_ctx {
     int ar_blocks_tap_only = 32;   // n == 1: the kernel is only the PCIe tap; leave SMs free
     int adamw_impl = 2;            // 0 vectorised, 1 TMA bulk-copy staged, 2 warp-tiled (measured best)
     int ar_impl = 0;               // 0 unrolled two-shot, 1 software-pipelined (one block per SM)
-    int zero1_impl = 1;            // ZeRO-1 AdamW + AG: 1 two groups per thread in flight, 0 one
+    int zero1_impl = 1;            // ZeRO-1 AdamW + AG: 1 two groups per thread in flight, 0 one,
+                                   // 2 tiles pushed by bulk copies (cp.async.bulk)
     int ar_pipe_blocks = 148;
     int tma_blocks = 148;
     int wt_blocks = 296;
@@ -475,6 +477,19 @@ static cm_status launch_adamw(cm_ctx* c, const AdamParams& P, int blocks, cudaSt
 }
 
 template <typename G, int OPT>
+static void launch_zero1_tma_t(int n, int grid, cudaStream_t s, const Zero1Params& Z) {
+    switch (n) {
+        case 1: adamw_zero1_tma_kernel<G, 1, OPT><<<grid, kZ1TmaThreads, 0, s>>>(Z); break;
+        case 2: adamw_zero1_tma_kernel<G, 2, OPT><<<grid, kZ1TmaThreads, 0, s>>>(Z); break;
+        case 3: adamw_zero1_tma_kernel<G, 3, OPT><<<grid, kZ1TmaThreads, 0, s>>>(Z); break;
+        case 4: adamw_zero1_tma_kernel<G, 4, OPT><<<grid, kZ1TmaThreads, 0, s>>>(Z); break;
+        case 5: adamw_zero1_tma_kernel<G, 5, OPT><<<grid, kZ1TmaThreads, 0, s>>>(Z); break;
+        case 6: adamw_zero1_tma_kernel<G, 6, OPT><<<grid, kZ1TmaThreads, 0, s>>>(Z); break;
+        case 7: adamw_zero1_tma_kernel<G, 7, OPT><<<grid, kZ1TmaThreads, 0, s>>>(Z); break;
+        default: adamw_zero1_tma_kernel<G, 8, OPT><<<grid, kZ1TmaThreads, 0, s>>>(Z); break;
+    }
+}
+template <typename G, int OPT>
 static void launch_zero1_t(int n, int grid, cudaStream_t s, const Zero1Params& Z) {
     switch (n) {
         case 1: adamw_zero1_kernel<G, 1, OPT><<<grid, 256, 0, s>>>(Z); break;
@@ -488,6 +503,19 @@ static void launch_zero1_t(int n, int grid, cudaStream_t s, const Zero1Params& Z
     }
 }
 static void launch_zero1(cm_ctx* c, const Zero1Params& Z, int grid, cudaStream_t s) {
+    if (c->zero1_impl == 2) {   // tiles of kZ1TmaTile elements, pushed by bulk copies
+        int64_t tiles = 0;
+        for (const auto& B : c->buckets) tiles += (B.padded / c->n + kZ1TmaTile - 1) / kZ1TmaTile;
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->zero1_tma_blocks));
+        if (Z.rec_kind == kOptSgd) {
+            if (c->dtype == CM_F32) launch_zero1_tma_t<F32Tag, kOptSgd>(c->n, g, s, Z);
+            else launch_zero1_tma_t<BF16Tag, kOptSgd>(c->n, g, s, Z);
+        } else {
+            if (c->dtype == CM_F32) launch_zero1_tma_t<F32Tag, kOptAdamW>(c->n, g, s, Z);
+            else launch_zero1_tma_t<BF16Tag, kOptAdamW>(c->n, g, s, Z);
+        }
+        return;
+    }
     if (Z.rec_kind == kOptSgd) {
         if (c->dtype == CM_F32) launch_zero1_t<F32Tag, kOptSgd>(c->n, grid, s, Z);
         else launch_zero1_t<BF16Tag, kOptSgd>(c->n, grid, s, Z);
@@ -590,7 +618,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "numa_node" && value >= -2 && value < 64 && !c->seg) c->numa_req = (int)value;
     else if (k == "drain_flush_bytes" && value >= 0 && value <= kDrainCoalesce) c->drain_flush = value;
     else if (k == "ar_impl" && (value == 0 || value == 1)) c->ar_impl = (int)value;
-    else if (k == "zero1_impl" && (value == 0 || value == 1)) c->zero1_impl = (int)value;
+    else if (k == "zero1_impl" && value >= 0 && value <= 2) c->zero1_impl = (int)value;
     else if (k == "ar_pipe_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_pipe_blocks = (int)value;
     // cost decomposition only (tools/model_mode.py): the staged tap's copy-engine drain is not
     // issued, so the ring is never written -- restore and the host-ring fallback are invalid
@@ -753,6 +781,9 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
     int zocc = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&zocc, adamw_zero1_kernel<F32Tag, 8>, 256, 0);
     c->zero1_blocks = std::min(c->sms * std::max(zocc, 1), kMaxBarrierBlocks);
+    int ztocc = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ztocc, adamw_zero1_tma_kernel<F32Tag, 8>, kZ1TmaThreads, 0);
+    c->zero1_tma_blocks = std::min(c->sms * std::max(ztocc, 1), kMaxBarrierBlocks);
     int wocc = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wocc, adamw_wt_kernel<F32Tag>, kAdamThreads, 0);
     c->wt_blocks = c->sms * std::max(wocc, 1);

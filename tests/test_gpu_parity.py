@@ -502,14 +502,14 @@ def _zero1_shard_of(flat, plan, rank):
     return np.concatenate(out)
 
 
-@pytest.mark.parametrize("zimpl", [1, 0])
+@pytest.mark.parametrize("zimpl", [1, 0, 2])
 @pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
 def test_zero1_bit_exact(n, dtype, zimpl):
     """ZeRO-1 (f3): reduce-scatter + tap, AdamW on the own shard, fused parameter
     all-gather.  Every rank's full p, its shard-local m/v and the shadow equal the oracle
-    (the unsharded definition) bit for bit, with two groups per thread in flight (default)
-    and with one (ablation)."""
+    (the unsharded definition) bit for bit, with two groups per thread in flight (default),
+    with one, and with the parameter all-gather pushed by bulk copies (zero1_impl 2)."""
     numel = TABLES["mixed"]
     g = make_group(numel, n, dtype, flags=cm.CM_FLAG_ZERO1)
     for r in g.ranks:
