@@ -310,8 +310,9 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
 /* cm_set_param -- tuning knobs used by benchmarks and ablations (defaults are the
  * measured best); CM_ERR_ARG for an unknown key or out-of-range value.
  *   "adamw_impl"          AdamW data movement (same arithmetic): 0 per-thread 128-bit items,
- *                         1 TMA bulk-copy staged, 2 warp-tiled 512-byte runs (default; 97.6%
- *                         of measured HBM copy bandwidth on B200 vs 82% / 77%)
+ *                         1 TMA bulk-copy staged, 2 warp-tiled 512-byte runs (default; at
+ *                         the measured HBM copy bandwidth on B200 vs 82% / 77%), 3 warp-tiled
+ *                         one tile per iteration with 4 blocks per SM (ablation)
  *   "adam_blocks"         grid cap of the training AdamW kernel
  *   "tma_blocks"          grid of the TMA AdamW kernel (default: one block per SM)
  *   "ar_blocks"           grid cap of the all-reduce kernel at n >= 2 (default: co-resident
