@@ -110,8 +110,12 @@ def run_arm(arm, args, rank, world, local):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     cur = torch.cuda.current_stream()
     a.record(cur)
+    lags = []
+    has_shadow = arm not in ("nccl",) and not (flags & (cm.CM_FLAG_NO_TAP | cm.CM_FLAG_NO_SHADOW))
     for i in range(args.warmup, args.warmup + args.steps):
         it(i)
+        if has_shadow:   # training steps issued minus the step the shadow has published
+            lags.append(cd.t - cd.r.ctx.info().shadow_step)
     for s in streams:
         cur.wait_stream(s)
     b.record(cur)
@@ -122,6 +126,11 @@ def run_arm(arm, args, rank, world, local):
     ok = cleanup()
     del model
     torch.cuda.empty_cache()
-    return {"ms_per_iter": ms.item(), "shadow_bit_identical": ok, "drain_ctas": drain}
+    out = {"ms_per_iter": ms.item(), "shadow_bit_identical": ok, "drain_ctas": drain}
+    if lags:
+        out["shadow_lag_iters"] = {"max": max(lags), "mean": sum(lags) / len(lags),
+                                   "what": "steps the host has issued minus the step the shadow published, "
+                                           "sampled after each timed iteration is issued (rank 0)"}
+    return out
 
 
