@@ -95,6 +95,11 @@ typedef enum { CM_SHADOW_HOST = 0, CM_SHADOW_DEVICE = 1 } cm_shadow_place;
                                          (rank 0) and hands it to the peers over a local Unix
                                          socket; CM_ERR_CONFIG if the box has no multicast
                                          support.  Multi-process ranks only.  Same bits.    */
+#define CM_FLAG_OVERWRITE (1ull << 7) /* create the shadow segment even if one of that name exists
+                                         (it is deleted first).  Without it, cm_connect refuses
+                                         (CM_ERR_STATE) to replace a surviving segment: after a
+                                         hard kill it is the only restore source (attach it with
+                                         CM_FLAG_ATTACH instead)                            */
 #define CM_FLAG_NO_SHADOW (1ull << 3) /* benchmark mode (bucket sweep): tap into the ring but
                                          keep no shadow replica and no flow control; the ring
                                          is overwritten freely; shadow/verify/restore refuse */
@@ -280,8 +285,31 @@ cm_status cm_init_state(cm_ctx *ctx, uint64_t seed, void *stream);
 
 /* cm_verify -- bitwise compare this rank's shadow shard (current half) with shard r of
  * the training p, m, v.  Synchronises `stream`.  *mismatch = -1 if
- * equal, else the flat index of the first differing element; CM_ERR_INVARIANT then.   */
+ * equal, else the flat index of the first differing element; CM_ERR_INVARIANT then.
+ * Same as cm_verify_ex(ctx, CM_VERIFY_SHADOW, mismatch, NULL, stream).                 */
 cm_status cm_verify(cm_ctx *ctx, int64_t *mismatch, void *stream);
+
+/* cm_verify_ex -- the bytes that carry the paper's claim, checked bitwise against the
+ * training replica at its current step T ("identical ... to the 8th decimal",
+ * reading R18 bitwise).  Synchronises the device.  `scope` is a mask:
+ *   CM_VERIFY_SHADOW  the shadow's working state at its published step (must equal T) vs
+ *                     shard r of training p/m/v (+ the host snapshot half if it is at T)
+ *   CM_VERIFY_HOST    HOST placement: the restore source alone -- the newest host snapshot
+ *                     <= T rolled forward over the tapped ring slots with their recorded
+ *                     scalars (what cm_restore computes; every step must be recoverable from
+ *                     host memory) -- vs training p/m/v; chunked through library scratch
+ *   CM_VERIFY_RING    the ring slot of iteration T-1 (host memory, shard-local) vs the reduced
+ *                     gradients the training step consumed: shard r of the grad buffer (the
+ *                     caller must not have overwritten it since step T), or with ZeRO-1 the
+ *                     staging half
+ * Results: CM_OK, *mismatch = -1, *what = -1; or CM_ERR_INVARIANT with *mismatch = the
+ * smallest differing flat index and *what = 0 p, 1 m, 2 v, 3 ring gradient; *what = 4: a
+ * kernel reported a non-finite value (*mismatch = its flat index, -1 unknown); *what = 5:
+ * the host log cannot reach step T (a gap).  CM_ERR_STATE if the shadow is not at T.     */
+#define CM_VERIFY_SHADOW 1
+#define CM_VERIFY_HOST 2
+#define CM_VERIFY_RING 4
+cm_status cm_verify_ex(cm_ctx *ctx, int32_t scope, int64_t *mismatch, int32_t *what, void *stream);
 
 /* Introspection (host-only, cheap). */
 typedef struct {
@@ -295,6 +323,12 @@ typedef struct {
     int64_t shadow_step;                /* last step the shadow published                 */
     int64_t launches;                   /* kernels this context launched so far           */
     uint64_t layout_hash;
+    int64_t nonfinite_step;             /* first step flagged non-finite, -1 none (cm_verify_ex) */
+    int64_t nonfinite_index;            /* a flat element index of that step, -1 unknown       */
+    int32_t persist_every;              /* K in effect (host shadows across processes: >= 2)   */
+    int32_t pad0;
+    int64_t host_half_step[2];          /* step held by each snapshot half (HOST: the host halves;
+                                           DEVICE: the HBM halves), -1 invalid              */
 } cm_info;
 cm_status cm_get_info(const cm_ctx *ctx, cm_info *out);
 cm_status cm_bucket_info(const cm_ctx *ctx, int32_t bucket, int64_t *elem_off, int64_t *padded,

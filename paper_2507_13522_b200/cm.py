@@ -15,6 +15,9 @@ CM_OK, CM_ERR_ARG, CM_ERR_CONFIG, CM_ERR_INVARIANT, CM_ERR_UNRECOVERABLE, CM_ERR
 STATUS_NAMES = {0: "CM_OK", 1: "CM_ERR_ARG", 2: "CM_ERR_CONFIG", 3: "CM_ERR_INVARIANT",
                 4: "CM_ERR_UNRECOVERABLE", 5: "CM_ERR_CUDA", 6: "CM_ERR_STATE"}
 CM_F32, CM_BF16 = 0, 1
+CM_VERIFY_SHADOW, CM_VERIFY_HOST, CM_VERIFY_RING = 1, 2, 4
+CM_VERIFY_ALL = CM_VERIFY_SHADOW | CM_VERIFY_HOST | CM_VERIFY_RING
+VERIFY_WHAT = {-1: None, 0: "p", 1: "m", 2: "v", 3: "ring", 4: "nonfinite", 5: "log_gap"}
 CM_SHADOW_HOST, CM_SHADOW_DEVICE = 0, 1
 CM_FLAG_NO_TAP = 1 << 0
 CM_FLAG_ATTACH = 1 << 1
@@ -23,11 +26,12 @@ CM_FLAG_NO_SHADOW = 1 << 3
 CM_FLAG_ZERO1 = 1 << 5          # sharded AdamW state + fused parameter all-gather
 CM_FLAG_TAP_DIRECT = 1 << 4     # default tap is "staged" (HBM staging + copy-engine drain)
 CM_FLAG_NVLS = 1 << 6           # one-shot push through an NVLink-SHARP multicast inbox
+CM_FLAG_OVERWRITE = 1 << 7      # replace a surviving shadow segment (else CM_ERR_STATE)
 
 # every symbol include/cm.h declares (tests check the library exports all of them)
 EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
            "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step",
-           "cm_apply_step_sgd", "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_get_info",
+           "cm_apply_step_sgd", "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_verify_ex", "cm_get_info",
            "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_set_param", "cm_join", "cm_shadow_save", "cm_shadow_load",
            "cm_crc32"]
 
@@ -57,7 +61,8 @@ class cm_info(C.Structure):
                 ("ring_depth", C.c_int32), ("grad_dtype", C.c_int32), ("shadow_place", C.c_int32),
                 ("peers_in_process", C.c_int32), ("drain_ctas", C.c_int32), ("numa_node", C.c_int32), ("padded_numel", C.c_int64),
                 ("shard_numel", C.c_int64), ("shadow_step", C.c_int64), ("launches", C.c_int64),
-                ("layout_hash", C.c_uint64)]
+                ("layout_hash", C.c_uint64), ("nonfinite_step", C.c_int64), ("nonfinite_index", C.c_int64),
+                ("persist_every", C.c_int32), ("pad0", C.c_int32), ("host_half_step", C.c_int64 * 2)]
 
 
 class CMError(RuntimeError):
@@ -95,6 +100,7 @@ def lib():
         L.cm_gen_grads.argtypes = [P, C.c_uint64, C.c_int64, C.c_int32, P]
         L.cm_init_state.argtypes = [P, C.c_uint64, P]
         L.cm_verify.argtypes = [P, C.POINTER(C.c_int64), P]
+        L.cm_verify_ex.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32), P]
         L.cm_get_info.argtypes = [P, C.POINTER(cm_info)]
         L.cm_bucket_info.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.cm_shadow_view.argtypes = [P, C.c_int32, C.POINTER(P), C.POINTER(P), C.POINTER(P)]
@@ -230,6 +236,16 @@ class Context:
         if st not in (CM_OK, CM_ERR_INVARIANT):
             self._check(st)
         return out.value
+
+    def verify_ex(self, scope=CM_VERIFY_ALL, stream=None):
+        """cm_verify_ex -> (status, mismatch flat index or -1, what: None/'p'/'m'/'v'/'ring'/
+        'nonfinite'/'log_gap').  CM_OK and CM_ERR_INVARIANT are returned, others raise."""
+        out = C.c_int64(-2)
+        what = C.c_int32(-2)
+        st = lib().cm_verify_ex(self._ctx, int(scope), C.byref(out), C.byref(what), _stream_ptr(stream))
+        if st not in (CM_OK, CM_ERR_INVARIANT):
+            self._check(st)
+        return st, out.value, VERIFY_WHAT.get(what.value, what.value)
 
     def info(self) -> cm_info:
         i = cm_info()

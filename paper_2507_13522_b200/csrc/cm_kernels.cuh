@@ -84,6 +84,49 @@ __device__ __forceinline__ void block_barrier(const Pads& pads, int n, int rank,
     __syncthreads();
 }
 
+// ------------------------------------------------------------------ non-finite detection
+// SPEC.md:313, 322 ("non-finite input -> numeric error"); SURVEY 8.b (CM_ERR_INVARIANT) and
+// reading R16.  Every kernel that produces a value of the path (the reduced sum, the updated
+// p/m/v) checks it; the common case is one untaken branch per vector.  A hit is reported into
+// a host-mapped pair nf[0] = step, nf[1] = flat element index (the segment header, so it
+// survives the process: restore never rolls forward over a flagged step).  Plain stores, no
+// atomics on host memory: an earlier (smaller) step is never overwritten by a later one;
+// writers of one step race benignly (any offending index of that step is reported, with a
+// flat index from the all-reduce / training kernels preferred over an unknown one, -1).
+__device__ __forceinline__ bool nonfinite_f32(float x) { return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u; }
+__device__ __forceinline__ bool nonfinite_bf16(uint32_t h) { return (h & 0x7f80u) == 0x7f80u; }
+__device__ __noinline__ void nf_report(volatile int64_t* nf, int64_t step, int64_t index) {
+    const int64_t cur = nf[0];
+    if (cur >= 0 && (cur < step || (cur == step && (index < 0 || nf[1] >= 0)))) return;
+    nf[1] = index;
+    __threadfence_system();
+    nf[0] = step;
+    __threadfence_system();
+}
+// updated state of 4 consecutive elements (index idx0..idx0+3; -1: unknown)
+__device__ __forceinline__ void nf_check4(volatile int64_t* nf, int64_t step, int64_t idx0, const float4& p,
+                                          const float4& m, const float4& v) {
+    if (!nf) return;
+    const float a[4] = {p.x, p.y, p.z, p.w}, b[4] = {m.x, m.y, m.z, m.w}, c[4] = {v.x, v.y, v.z, v.w};
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) any |= nonfinite_f32(a[k]) | nonfinite_f32(b[k]) | nonfinite_f32(c[k]);
+    if (!any) return;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (nonfinite_f32(a[k]) | nonfinite_f32(b[k]) | nonfinite_f32(c[k])) {
+            nf_report(nf, step, idx0 < 0 ? -1 : idx0 + k);
+            return;
+        }
+}
+// a stream-ordered kernel of a step that must not run once the step (or an earlier one) was
+// flagged: the shadow never applies or publishes a non-finite iteration
+__device__ __forceinline__ bool nf_blocked(const volatile int64_t* skip, int64_t step) {
+    if (!skip) return false;
+    const int64_t s = skip[0];
+    return s >= 0 && s <= step;
+}
+
 // ------------------------------------------------------------------ dtype traits
 // A 16-byte vector of gradients: 4 fp32 or 8 bf16.
 struct F32Tag {};
@@ -216,7 +259,33 @@ struct ArParams {
     unsigned long long done_target;
     volatile uint64_t* tap_flag;   // host-mapped (slot, bucket, rank) flag; nullptr: none
     uint64_t tap_flag_value;       // iteration + 1
+    volatile int64_t* nf;          // non-finite report (host-mapped step, index); nullptr: off
+    int64_t elem0;                 // flat element index of the shard's first element
+    int64_t nf_step;               // the step that applies this reduce (iteration + 1)
 };
+
+// a reduced 16-byte vector (the value the tap and the all-gather store) is finite?  Else
+// report the first non-finite element (flat index elem0 + q*V + k).
+template <typename G>
+__device__ __forceinline__ void nf_check_vec(volatile int64_t* nf, int64_t step, int64_t elem0, const uint4& r) {
+    if (!nf) return;
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+    if constexpr (std::is_same<G, F32Tag>::value) {
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) any |= nonfinite_f32(__uint_as_float(w[k]));
+        if (!any) return;
+        for (int k = 0; k < 4; ++k)
+            if (nonfinite_f32(__uint_as_float(w[k]))) { nf_report(nf, step, elem0 + k); return; }
+    } else {
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) any |= nonfinite_bf16(w[k] & 0xFFFFu) | nonfinite_bf16(w[k] >> 16);
+        if (!any) return;
+        for (int k = 0; k < 8; ++k)
+            if (nonfinite_bf16((w[k >> 1] >> (16 * (k & 1))) & 0xFFFFu)) { nf_report(nf, step, elem0 + k); return; }
+    }
+}
 
 template <typename G, int N>
 __device__ __forceinline__ uint4 reduce_vec(const uint4 (&x)[N]) {
@@ -261,6 +330,7 @@ template <typename G, int N>
 __device__ __forceinline__ void ar_reduce_store(const ArParams& P, int64_t q, const uint4 (&x)[N]) {
     const uint4 r = reduce_vec<G, N>(x);
     const int64_t off = q * 16;
+    nf_check_vec<G>(P.nf, P.nf_step, P.elem0 + q * GT<G>::kPerVec, r);
     if (P.tap) st_cs_v4(P.tap + off, r);
     if (P.ag) {
 #pragma unroll
@@ -363,6 +433,9 @@ struct OsParams {
     unsigned long long done_target;
     volatile uint64_t* tap_flag;
     uint64_t tap_flag_value;
+    volatile int64_t* nf;          // non-finite report (see ArParams)
+    int64_t elem0;                 // flat element index of the bucket's first element
+    int64_t nf_step;
 };
 
 constexpr int kOsThreads = 256;
@@ -394,6 +467,7 @@ __global__ void __launch_bounds__(kOsThreads) os_tap_kernel(const OsParams P) {
 #pragma unroll
         for (int k = 0; k < N; ++k) x[k] = ld_v4((k == P.rank ? (const char*)P.own : P.inbox[k]) + q * 16);
         const uint4 r = reduce_vec<G, N>(x);
+        nf_check_vec<G>(P.nf, P.nf_step, P.elem0 + q * GT<G>::kPerVec, r);
         if (!P.rs_only) st_v4(P.own + q * 16, r);
         if (P.tap && q >= P.shard_lo && q < P.shard_hi) st_cs_v4(P.tap + (q - P.shard_lo) * 16, r);
     }
@@ -492,7 +566,22 @@ struct AdamParams {
     Pads pads;
     uint32_t epoch;
     int fence_n, fence_rank;       // fence_n = 0: no fence
+    volatile int64_t* nf;          // non-finite report of the updated state (nullptr: off)
+    int64_t nf_base;               // flat index of element 0 of this launch (-1: not flat, e.g. shadow)
+    const volatile int64_t* skip_nf;  // shadow: do nothing if the step (or an earlier) was flagged
 };
+
+// whole-block early exit of a shadow kernel whose step was flagged non-finite (one host read
+// per block)
+template <typename PT>
+__device__ __forceinline__ bool block_nf_blocked(const PT& P) {
+    if (!P.skip_nf) return false;
+    __shared__ int blk;
+    if (threadIdx.x == 0) blk = nf_blocked(P.skip_nf, P.step) ? 1 : 0;
+    __syncthreads();
+    return blk != 0;
+}
+__device__ __forceinline__ int64_t nf_idx(int64_t base, int64_t e) { return base < 0 ? -1 : base + e; }
 
 // the step's scalars into the host-mapped ring-slot record, then its tag (one thread)
 template <typename PT>
@@ -529,6 +618,8 @@ __device__ __forceinline__ void adamw_item(const AdamParams& P, int64_t e) {
     adamw_elem(g0.z, P.s, p0.z, m0.z, v0.z); adamw_elem(g0.w, P.s, p0.w, m0.w, v0.w);
     adamw_elem(g1.x, P.s, p1.x, m1.x, v1.x); adamw_elem(g1.y, P.s, p1.y, m1.y, v1.y);
     adamw_elem(g1.z, P.s, p1.z, m1.z, v1.z); adamw_elem(g1.w, P.s, p1.w, m1.w, v1.w);
+    nf_check4(P.nf, P.step, nf_idx(P.nf_base, e), p0, m0, v0);
+    nf_check4(P.nf, P.step, nf_idx(P.nf_base, e + 4), p1, m1, v1);
     __stcs(reinterpret_cast<float4*>(P.p_out + e), p0);
     __stcs(reinterpret_cast<float4*>(P.p_out + e + 4), p1);
     __stcs(reinterpret_cast<float4*>(P.m_out + e), m0);
@@ -539,6 +630,7 @@ __device__ __forceinline__ void adamw_item(const AdamParams& P, int64_t e) {
 
 template <typename G>
 __global__ void __launch_bounds__(kAdamThreads) adamw_kernel(const AdamParams P) {
+    if (block_nf_blocked(P)) return;
     const int64_t items = P.n / 8;
     const int64_t stride = (int64_t)gridDim.x * kAdamThreads;
     int64_t q = blockIdx.x * (int64_t)kAdamThreads + threadIdx.x;
@@ -555,6 +647,8 @@ __global__ void __launch_bounds__(kAdamThreads) adamw_kernel(const AdamParams P)
             else R = __uint_as_float(((uint32_t)((const uint16_t*)P.g)[e]) << 16);
             float p = P.p_in[e], m = P.m_in[e], v = P.v_in[e];
             adamw_elem(R, P.s, p, m, v);
+            nf_check4(P.nf, P.step, nf_idx(P.nf_base, e), make_float4(p, 0.f, 0.f, 0.f), make_float4(m, 0.f, 0.f, 0.f),
+                      make_float4(v, 0.f, 0.f, 0.f));
             P.p_out[e] = p; P.m_out[e] = m; P.v_out[e] = v;
         }
     }
@@ -594,6 +688,7 @@ __device__ __forceinline__ void wt_compute_store(const AdamParams& P, int64_t e,
         sgd_elem(g.z, P.q, p.z, m.z);
         sgd_elem(g.w, P.q, p.w, m.w);
     }
+    nf_check4(P.nf, P.step, nf_idx(P.nf_base, e), p, m, v);
     __stcs(reinterpret_cast<float4*>(P.p_out + e), p);
     __stcs(reinterpret_cast<float4*>(P.m_out + e), m);
     if constexpr (OPT == kOptAdamW) __stcs(reinterpret_cast<float4*>(P.v_out + e), v);
@@ -604,6 +699,7 @@ __device__ __forceinline__ void wt_compute_store(const AdamParams& P, int64_t e,
 // twice the warps to overlap one warp's IEEE div/sqrt chain with other warps' loads)
 template <typename G, int OPT, bool PAIR = true>
 __device__ __forceinline__ void wt_body(const AdamParams& P) {
+    if (block_nf_blocked(P)) return;
     if (P.fence_n) block_barrier(P.pads, P.fence_n, P.fence_rank, P.epoch, 0);
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)kAdamThreads + threadIdx.x) >> 5;
@@ -713,6 +809,7 @@ template <typename G>
 __global__ void __launch_bounds__(kTmaThreads, 1) adamw_tma_kernel(const AdamParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[kTmaStages];
+    if (block_nf_blocked(P)) return;
     constexpr int GB = GT<G>::kBytes;
     const int64_t ntiles = (P.n + kTmaTile - 1) / kTmaTile;
     auto stage_ptr = [&](int st) { return smem + (size_t)st * TmaTile<G>::kStageBytes; };
@@ -765,6 +862,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adamw_tma_kernel(const AdamPar
             adamw_elem(g.y, P.s, p.y, m.y, v.y);
             adamw_elem(g.z, P.s, p.z, m.z, v.z);
             adamw_elem(g.w, P.s, p.w, m.w, v.w);
+            nf_check4(P.nf, P.step, nf_idx(P.nf_base, e0 + q), p, m, v);
             *reinterpret_cast<float4*>(sp + q) = p;
             *reinterpret_cast<float4*>(sm + q) = m;
             *reinterpret_cast<float4*>(sv + q) = v;
@@ -814,6 +912,7 @@ struct Zero1Params {
     int32_t rec_kind;
     int64_t step;
     int unroll2;                    // 1: two groups per thread in flight (default), 0: one
+    volatile int64_t* nf;           // non-finite report (flat index)
 };
 
 // shard-local index j -> flat index of rank P.rank's element (b: running bucket index, j
@@ -851,6 +950,7 @@ __device__ __forceinline__ void z1_compute_store(const Zero1Params& P, int64_t j
         sgd_elem(g.z, P.q, p.z, m.z);
         sgd_elem(g.w, P.q, p.w, m.w);
     }
+    nf_check4(P.nf, P.step, flat, p, m, v);
     __stcs(reinterpret_cast<float4*>(P.m + j), m);
     const uint4 pw = make_uint4(__float_as_uint(p.x), __float_as_uint(p.y), __float_as_uint(p.z),
                                 __float_as_uint(p.w));
@@ -948,6 +1048,7 @@ __global__ void __launch_bounds__(kZ1TmaThreads) adamw_zero1_tma_kernel(const Ze
                 sgd_elem(g[u].z, P.q, p[u].z, m[u].z);
                 sgd_elem(g[u].w, P.q, p[u].w, m[u].w);
             }
+            nf_check4(P.nf, P.step, f0 + e, p[u], m[u], v[u]);
             __stcs(reinterpret_cast<float4*>(P.m + j0 + e), m[u]);
             *reinterpret_cast<float4*>(&tile[buf][e]) = p[u];
         }
@@ -1010,24 +1111,48 @@ __global__ void __launch_bounds__(256) shard_copy_kernel(const ShardCopyParams P
     if (P.dir == 1 && P.barriers) block_barrier(P.pads, P.n, P.rank, P.epoch, 1);
 }
 
-// bitwise compare shadow shard-local arrays with this rank's flat shard
+// Bitwise compare of shadow-side shard-local arrays (elements [j0, j0 + len) of the shard,
+// sp[0] = element j0) with this rank's training p/m/v.  first_bad = min over mismatches of
+// flat * 4 + what (what: 0 p, 1 m, 2 v), so the host learns the first flat index and array.
 __global__ void __launch_bounds__(256) compare_kernel(const float* __restrict__ sp, const float* __restrict__ sm,
                                                       const float* __restrict__ sv, const float* __restrict__ p,
                                                       const float* __restrict__ m, const float* __restrict__ v,
                                                       const BucketDev* __restrict__ buckets, int nb, int n,
-                                                      int rank, int64_t shard_n,
+                                                      int rank, int64_t j0, int64_t len,
                                                       unsigned long long* first_bad, int mv_local) {
+    int b = 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < len;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = j0 + q;
+        while (b + 1 < nb && j >= buckets[b + 1].shard_off) ++b;
+        const BucketDev B = buckets[b];
+        const int64_t flat = B.off + (int64_t)rank * (B.padded / n) + (j - B.shard_off);
+        const int64_t mi = mv_local ? j : flat;
+        int what = -1;
+        if (__float_as_uint(sv[q]) != __float_as_uint(v[mi])) what = 2;
+        if (__float_as_uint(sm[q]) != __float_as_uint(m[mi])) what = 1;
+        if (__float_as_uint(sp[q]) != __float_as_uint(p[flat])) what = 0;
+        if (what >= 0) atomicMin(first_bad, (unsigned long long)flat * 4ull + (unsigned long long)what);
+    }
+}
+
+// Bitwise compare of a tap ring slot (shard-local, read through its device alias) with the
+// reduced gradients the training step used: the flat grad buffer's shard r (ref_flat = 1) or
+// the shard-local staging half (ref_flat = 0, ZeRO-1).  Reports flat * 4 + 3.
+__global__ void __launch_bounds__(256) compare_grads_kernel(const void* ring, const void* ref, int ref_flat,
+                                                            const BucketDev* __restrict__ buckets, int nb, int n,
+                                                            int rank, int64_t shard_n, int es,
+                                                            unsigned long long* first_bad) {
     int b = 0;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < shard_n;
          j += (int64_t)gridDim.x * blockDim.x) {
         while (b + 1 < nb && j >= buckets[b + 1].shard_off) ++b;
         const BucketDev B = buckets[b];
         const int64_t flat = B.off + (int64_t)rank * (B.padded / n) + (j - B.shard_off);
-        const int64_t mi = mv_local ? j : flat;
-        if (__float_as_uint(sp[j]) != __float_as_uint(p[flat]) ||
-            __float_as_uint(sm[j]) != __float_as_uint(m[mi]) ||
-            __float_as_uint(sv[j]) != __float_as_uint(v[mi]))
-            atomicMin(first_bad, (unsigned long long)flat);
+        const int64_t ri = ref_flat ? flat : j;
+        const bool bad = es == 4 ? ((const volatile uint32_t*)ring)[j] != ((const uint32_t*)ref)[ri]
+                                 : ((const volatile uint16_t*)ring)[j] != ((const uint16_t*)ref)[ri];
+        if (bad) atomicMin(first_bad, (unsigned long long)flat * 4ull + 3ull);
     }
 }
 
@@ -1045,7 +1170,9 @@ __global__ void __launch_bounds__(256) drain_kernel(const uint4* __restrict__ sr
 }
 
 // stream-ordered store of one int64 into host-mapped memory (segment header)
-__global__ void publish_kernel(volatile int64_t* dst, int64_t value) {
+__global__ void publish_kernel(volatile int64_t* dst, int64_t value, const volatile int64_t* skip_nf,
+                               int64_t step) {
+    if (nf_blocked(skip_nf, step)) return;   // a flagged step is never published
     __threadfence_system();
     *dst = value;
     __threadfence_system();

@@ -43,7 +43,7 @@ using namespace cm;
 namespace {
 
 constexpr uint64_t kMagic = 0x434B4D5442323030ull;  // "CKMTB200"
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;   // 2: non-finite report in the header
 constexpr size_t kAlign = 4096;
 constexpr int kStages = 4;                       // shadow staging buffers
 constexpr int64_t kOsSlotBytes = 1ll << 20;      // one-shot inbox slot (largest one-shot bucket)
@@ -59,6 +59,10 @@ struct SegHeader {
     volatile int64_t shadow_step;   // last step published by the shadow
     volatile int64_t half_step[2];  // step held by each ping-pong half, -1 = invalid
     uint64_t meta_off, flags_off, ring_off, state_off, total;
+    // non-finite report (written by the kernels through the device alias): the first step
+    // whose reduced gradients or updated state held an inf/NaN, and a flat element index
+    // (-1: unknown).  -1 = none.  Restore never rolls forward to or past nf_step.
+    volatile int64_t nf_step, nf_index;
 };
 static_assert(sizeof(SegHeader) <= kAlign, "header");
 
@@ -191,6 +195,13 @@ struct cm_ctx {
     unsigned long long* d_done_ctr = nullptr;
     unsigned long long done_total = 0;
     unsigned long long* d_bad = nullptr;
+    // non-finite report pair (step, index): host view + device alias.  Points into the segment
+    // header once connected with a tap (it then survives the process), else into `ctl`.
+    int64_t* ctl = nullptr;               // pinned, mapped fallback pair
+    volatile int64_t* nf_host = nullptr;
+    volatile int64_t* nf_dev = nullptr;
+    // cm_verify_ex scratch (chunked host roll-forward): p, m, v chunks
+    float* vf_scratch = nullptr;
 
     // launch geometry
     int ar_blocks_max = 296, adam_blocks = 1184, shadow_blocks = 296, misc_blocks = 1184;
@@ -285,6 +296,19 @@ static cm_status fail(cm_ctx* c, cm_status s, const char* fmt, ...) {
 #define CHECK_LAUNCH() CU(cudaGetLastError())
 
 static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+// Sticky numeric error (reading R16): once a kernel reported a non-finite value, every
+// enqueueing call refuses with CM_ERR_INVARIANT until cm_restore rolls back to the last
+// finite step.  The report is read from host-mapped memory (no synchronisation), so it
+// surfaces at the first call after the flagging kernel ran; cm_verify always sees it.
+static cm_status check_nf(cm_ctx* c) {
+    if (!c->nf_host) return CM_OK;
+    const int64_t st = c->nf_host[0];
+    if (st < 0) return CM_OK;
+    return fail(c, CM_ERR_INVARIANT,
+                "non-finite value (inf/NaN) in step %lld at flat index %lld; the shadow stopped at the last "
+                "finite step: call cm_restore", (long long)st, (long long)c->nf_host[1]);
+}
 
 // ---------------------------------------------------------------- bucket planner
 // PAPER.md:258-264 (sec 4.2.2) with readings R10-R13 (see cm.h cm_plan_buckets).
@@ -533,10 +557,13 @@ static void set_step(AdamParams& P, const StepRec& r) {
     r.to_floats(P.rec);
 }
 
-static cm_status publish(cm_ctx* c, volatile int64_t* host_field, int64_t value, cudaStream_t s) {
+// skip_step >= 0: a conditional publication that does not happen once step skip_step (or an
+// earlier one) was flagged non-finite; -1: unconditional (invalidations)
+static cm_status publish(cm_ctx* c, volatile int64_t* host_field, int64_t value, cudaStream_t s,
+                         int64_t skip_step = -1) {
     // device alias of a header field
     volatile int64_t* d = (volatile int64_t*)(c->seg_dev + ((char*)host_field - c->seg));
-    publish_kernel<<<1, 1, 0, s>>>(d, value);
+    publish_kernel<<<1, 1, 0, s>>>(d, value, skip_step >= 0 ? c->nf_dev : nullptr, skip_step);
     c->launches++;
     CHECK_LAUNCH();
     return CM_OK;
@@ -723,6 +750,15 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
     CU(cudaMalloc(&c->d_done_ctr, sizeof(unsigned long long)));
     CU(cudaMemset(c->d_done_ctr, 0, sizeof(unsigned long long)));
     CU(cudaMalloc(&c->d_bad, sizeof(unsigned long long)));
+    CU(cudaHostAlloc((void**)&c->ctl, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    c->ctl[0] = -1;
+    c->ctl[1] = -1;
+    c->nf_host = c->ctl;
+    {
+        int64_t* d = nullptr;
+        CU(cudaHostGetDevicePointer((void**)&d, c->ctl, 0));
+        c->nf_dev = d;
+    }
     for (int i = 0; i < c->D; ++i) {
         cudaEvent_t a, b;
         CU(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
@@ -1072,6 +1108,20 @@ cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
     // them on one stream in order, so no kernel ever waits for another and no barrier is
     // needed (B200_PROFILING.md: never spin across launches on one GPU).
     c->barriers = !(all_local && same_dev);
+    // Hard-kill safety of a host shadow shared by several processes: restore needs one step
+    // that every shard can still reach.  When a rank's iteration-t kernel runs, every peer's
+    // ring already holds step t-1 (its staging half of t-2 was drained), so a peer may be stuck
+    // as low as t-1 (or t-2 while this shard persists step t over its older half).  This shard
+    // keeps that reachable only if its older snapshot is <= t-2 and the ring from it survives
+    // the overwrite of step t+1-D: K >= 2 and D >= K + 1.  Virtual
+    // ranks restore only after every stream is synchronised (all drains landed).
+    if (c->barriers && c->n > 1 && !c->no_tap && !c->no_shadow && c->shadow_place == CM_SHADOW_HOST) {
+        if (c->K < 2) c->K = 2;
+        if (c->D < c->K + 1)
+            return fail(c, CM_ERR_CONFIG,
+                        "host shadow across processes needs ring_depth >= persist_every + 1 (D=%d, K=%d): a "
+                        "hard kill could otherwise leave no step every shard can reach", c->D, c->K);
+    }
     for (int k = 0; k < c->n; ++k) {
         void* ptr[6];
         if (k == c->rank) {
@@ -1201,8 +1251,14 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
             return fail(c, CM_ERR_STATE, "attach: segment %s has size %zu, layout needs %zu", name,
                         (size_t)stt.st_size, (size_t)h.total);
     } else {
-        shm_unlink(name);
+        // A surviving segment is the only restore source after a hard kill: never delete it
+        // implicitly.  CM_FLAG_OVERWRITE states an intentional fresh start.
+        if (c->cfg.flags & CM_FLAG_OVERWRITE) shm_unlink(name);
         c->shm_fd = shm_open(name, O_RDWR | O_CREAT | O_EXCL, 0600);
+        if (c->shm_fd < 0 && errno == EEXIST)
+            return fail(c, CM_ERR_STATE,
+                        "shadow segment %s exists (a previous run's restore source): attach with CM_FLAG_ATTACH, "
+                        "or start fresh with CM_FLAG_OVERWRITE / cm_unlink_shadow", name);
         if (c->shm_fd < 0) return fail(c, CM_ERR_CONFIG, "shm_open(%s) failed: %s", name, strerror(errno));
         if (ftruncate(c->shm_fd, (off_t)h.total) != 0)
             return fail(c, CM_ERR_CONFIG, "ftruncate(%s, %zu) failed: %s", name, (size_t)h.total, strerror(errno));
@@ -1224,11 +1280,15 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
         c->hdr->shadow_step = -1;
         c->hdr->half_step[0] = -1;
         c->hdr->half_step[1] = -1;
+        c->hdr->nf_step = -1;
+        c->hdr->nf_index = -1;
         for (int i = 0; i < c->D; ++i) slot_meta(c, i)->step_tag = -1;
     }
     CU(cudaHostRegister(c->seg, c->seg_size, cudaHostRegisterMapped | cudaHostRegisterPortable));
     c->seg_registered = true;
     CU(cudaHostGetDevicePointer((void**)&c->seg_dev, c->seg, 0));
+    c->nf_host = &c->hdr->nf_step;    // the report now survives the process (restore reads it)
+    c->nf_dev = to_dev(c, &c->hdr->nf_step);
     if (c->no_shadow) return CM_OK;   // tap-only benchmark mode: ring + flags, no replica
     if (c->shadow_place == CM_SHADOW_HOST) {
         float* base = (float*)(c->seg + c->hdr->state_off);
@@ -1329,6 +1389,10 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     if (c->cuda_dead) return CM_ERR_CUDA;
     if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
     if (bucket < 0 || bucket >= (int32_t)c->buckets.size()) return fail(c, CM_ERR_ARG, "bucket %d out of range", bucket);
+    {
+        cm_status e = check_nf(c);
+        if (e != CM_OK) return e;
+    }
     cudaStream_t s = S(stream);
     if (t != c->cur_iter) {
         if (t == c->cur_iter + 1 && c->issued_count == (int)c->buckets.size()) {
@@ -1371,6 +1435,9 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     P.rank = c->rank;
     P.barriers = c->barriers ? 1 : 0;
     P.ag = (c->n > 1 && !c->zero1) ? 1 : 0;   // ZeRO-1 gathers the updated params instead
+    P.nf = c->nf_dev;                          // non-finite reduced values -> CM_ERR_INVARIANT
+    P.elem0 = B.off + (int64_t)c->rank * shard;
+    P.nf_step = t + 1;
     // exit barrier only when the training step does not fence the iteration: ZeRO-1's
     // optimizer ends in a barrier; the replicated AdamW starts with one when lazy_exit
     P.exit_barrier = (c->lazy_exit || c->zero1) ? 0 : 1;
@@ -1437,6 +1504,9 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         O.pads = c->pads;
         O.epoch = P.epoch;
         O.rank = c->rank;
+        O.nf = c->nf_dev;
+        O.elem0 = B.off;
+        O.nf_step = t + 1;
         const int og = (int)std::max<int64_t>(1, std::min<int64_t>((O.nvec + kOsThreads - 1) / kOsThreads,
                                                                    kMaxBarrierBlocks));
         if (fused_tap) {
@@ -1536,6 +1606,10 @@ static cm_status step_checks(cm_ctx* c, int64_t step, int kind) {
     if (c->cur_iter != step - 1 || c->issued_count != (int)c->buckets.size())
         return fail(c, CM_ERR_STATE, "step %lld before all buckets of iteration %lld were all-reduced (%d/%zu)",
                     (long long)step, (long long)(step - 1), c->issued_count, c->buckets.size());
+    {
+        cm_status e = check_nf(c);
+        if (e != CM_OK) return e;
+    }
     if (c->opt_kind >= 0 && c->opt_kind != kind)
         return fail(c, CM_ERR_STATE, "optimizer changed mid-run (%s after %s steps): m/v would change meaning",
                     kind == kOptSgd ? "SGD" : "AdamW", c->opt_kind == kOptSgd ? "SGD" : "AdamW");
@@ -1598,6 +1672,9 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
     P.p_out = c->p; P.m_out = c->m; P.v_out = c->v;
     P.n = c->P_pad;
     set_step(P, rec);
+    P.step = step;
+    P.nf = c->nf_dev;       // non-finite updated state -> CM_ERR_INVARIANT
+    P.nf_base = 0;
     if (!c->no_tap) {
         SlotMeta* sm = slot_meta(c, slot);
         P.hp_rec = to_dev(c, sm->sc);
@@ -1623,6 +1700,7 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
         Z.epoch = ++c->epoch;
         Z.hp_rec = P.hp_rec; Z.hp_kind = P.hp_kind; Z.hp_tag = P.hp_tag; Z.step = step;
         Z.unroll2 = c->zero1_impl;
+        Z.nf = c->nf_dev;
         memcpy(Z.rec, P.rec, sizeof Z.rec);
         Z.rec_kind = P.rec_kind;
         const int64_t want = (Z.L / 4 + 255) / 256;
@@ -1735,6 +1813,10 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
             set_step(P, rec);
             P.p_in = c->sd[hin][0] + lo; P.m_in = c->sd[hin][1] + lo; P.v_in = c->sd[hin][2] + lo;
             P.p_out = c->sd[hout][0] + lo; P.m_out = c->sd[hout][1] + lo; P.v_out = c->sd[hout][2] + lo;
+            P.step = step;
+            P.nf = c->nf_dev;       // the shadow checks its own results too (index unknown: -1)
+            P.nf_base = -1;
+            P.skip_nf = c->nf_dev;  // and never applies a flagged step
             st = launch_adamw(c, P, c->shadow_blocks, c->cs_k);
             if (st != CM_OK) return st;
             CU(cudaEventRecord(c->ev_stg_free[j], c->cs_k));
@@ -1759,12 +1841,12 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
         }
     }
     if (!host || persist) {
-        st = publish(c, hs, step, s);
+        st = publish(c, hs, step, s, step);   // not if the step was flagged non-finite
         if (st != CM_OK) return st;
     }
     if (persist) c->hh_step[ph] = step;
     if (persisted) *persisted = persist;
-    return publish(c, &c->hdr->shadow_step, step, s);
+    return publish(c, &c->hdr->shadow_step, step, s, step);
 }
 
 cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
@@ -1772,6 +1854,10 @@ cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
     if (c->cuda_dead) return CM_ERR_CUDA;
     if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
     if (c->no_tap || c->no_shadow) return fail(c, CM_ERR_STATE, "context has no shadow (CM_FLAG_NO_TAP/NO_SHADOW)");
+    {
+        cm_status e = check_nf(c);
+        if (e != CM_OK) return e;
+    }
     if (step != c->shadow_enq + 1)
         return fail(c, CM_ERR_STATE, "shadow step %lld after %lld: iteration gap", (long long)step, (long long)c->shadow_enq);
     const int slot = (int)((step - 1) % c->D);
@@ -1850,40 +1936,101 @@ cm_status cm_init_state(cm_ctx* c, uint64_t seed, void* stream) {
     return CM_OK;
 }
 
-cm_status cm_verify(cm_ctx* c, int64_t* mismatch, void* stream) {
+static cm_status verify_host_log(cm_ctx* c, int64_t T, cudaStream_t s, int64_t* gap_from);
+static bool slot_complete(const char* base, const SegHeader* h, int D, int nb, int64_t s);
+
+// Bitwise checks of the checkpoint against the training replica (PAPER.md:605,
+// SPEC.md:588-596).  See cm.h for the scopes.  Synchronous; reports the first flat index.
+cm_status cm_verify_ex(cm_ctx* c, int32_t scope, int64_t* mismatch, int32_t* what, void* stream) {
     if (!c || !mismatch) return CM_ERR_ARG;
+    *mismatch = -1;
+    if (what) *what = -1;
     if (c->cuda_dead) return CM_ERR_CUDA;
     if (!c->connected || c->no_tap || c->no_shadow) return fail(c, CM_ERR_STATE, "no shadow to verify");
+    if (scope <= 0 || scope > (CM_VERIFY_SHADOW | CM_VERIFY_HOST | CM_VERIFY_RING)) return fail(c, CM_ERR_ARG, "bad scope");
     cudaStream_t s = S(stream);
     CU(cudaStreamSynchronize(s));
     CU(cudaDeviceSynchronize());
+    if (c->nf_host[0] >= 0) {
+        *mismatch = c->nf_host[1];
+        if (what) *what = 4;
+        return check_nf(c);
+    }
+    const int64_t T = c->train_step;
     const int64_t step = c->hdr->shadow_step;
     if (step < 0) return fail(c, CM_ERR_STATE, "shadow has no published step");
-    const int h = (int)(step & 1);
     unsigned long long init = ~0ull;
     CU(cudaMemcpy(c->d_bad, &init, sizeof init, cudaMemcpyHostToDevice));
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->shard_numel + 255) / 256, c->misc_blocks));
-    // the HBM working half, and (HOST placement) the persisted host snapshot if it is at
-    // the same step (with persist_every K > 1 it may be older; restore rolls it forward)
-    int hhalf = -1;
-    if (c->shadow_place == CM_SHADOW_HOST)
-        for (int i = 0; i < 2; ++i)
-            if (c->hdr->half_step[i] == step) hhalf = i;
-    for (int which = 0; which < (hhalf >= 0 ? 2 : 1); ++which) {
-        const float* src[3];
-        for (int a = 0; a < 3; ++a) src[a] = which == 0 ? c->sd[h][a] : to_dev(c, c->sh[hhalf][a]);
-        compare_kernel<<<grid, 256, 0, s>>>(src[0], src[1], src[2], c->p, c->m, c->v, c->d_buckets,
-                                            (int)c->buckets.size(), c->n, c->rank, c->shard_numel, c->d_bad,
-                                            c->zero1 ? 1 : 0);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->shard_numel + 255) / 256, c->misc_blocks));
+    if (scope & CM_VERIFY_SHADOW) {
+        if (step != T)
+            return fail(c, CM_ERR_STATE, "shadow published step %lld, training is at step %lld", (long long)step,
+                        (long long)T);
+        // the HBM working half, and (HOST placement) the persisted host snapshot if it is at
+        // the same step (with persist_every K > 1 it is usually older: CM_VERIFY_HOST)
+        const int h = (int)(step & 1);
+        int hhalf = -1;
+        if (c->shadow_place == CM_SHADOW_HOST)
+            for (int i = 0; i < 2; ++i)
+                if (c->hdr->half_step[i] == step) hhalf = i;
+        for (int which = 0; which < (hhalf >= 0 ? 2 : 1); ++which) {
+            const float* src[3];
+            for (int a = 0; a < 3; ++a) src[a] = which == 0 ? c->sd[h][a] : to_dev(c, c->sh[hhalf][a]);
+            compare_kernel<<<grid, 256, 0, s>>>(src[0], src[1], src[2], c->p, c->m, c->v, c->d_buckets,
+                                                (int)c->buckets.size(), c->n, c->rank, 0, c->shard_numel, c->d_bad,
+                                                c->zero1 ? 1 : 0);
+            c->launches++;
+            CHECK_LAUNCH();
+        }
+    }
+    if ((scope & CM_VERIFY_RING) && T >= 1) {
+        // the tapped gradients of iteration T-1 (ring slot (T-1) mod D, shard-local, host memory)
+        // vs what the training step consumed: shard r of the grad buffer (the caller has not
+        // overwritten it since the step), or with ZeRO-1 the staging half it read
+        const int slot = (int)((T - 1) % c->D);
+        if (!slot_complete(c->seg, c->hdr, c->D, (int)c->buckets.size(), T)) {
+            *mismatch = -1;
+            if (what) *what = 5;
+            return fail(c, CM_ERR_INVARIANT, "ring slot %d does not hold a complete step %lld", slot, (long long)T);
+        }
+        const void* ref = c->grad;
+        int ref_flat = 1;
+        if (c->zero1) {
+            const int hh = (int)((T - 1) & 1);
+            if (c->stage_iter[hh] != T - 1) return fail(c, CM_ERR_STATE, "ZeRO-1 staging half was reused");
+            ref = c->stage_buf[hh];
+            ref_flat = 0;
+        }
+        compare_grads_kernel<<<grid, 256, 0, s>>>(ring_slot_dev(c, slot), ref, ref_flat, c->d_buckets,
+                                                  (int)c->buckets.size(), c->n, c->rank, c->shard_numel, c->es,
+                                                  c->d_bad);
         c->launches++;
         CHECK_LAUNCH();
+    }
+    if ((scope & CM_VERIFY_HOST) && c->shadow_place == CM_SHADOW_HOST) {
+        int64_t gap = -1;
+        cm_status st = verify_host_log(c, T, s, &gap);
+        if (st != CM_OK) return st;
+        if (gap >= 0) {
+            if (what) *what = 5;
+            return fail(c, CM_ERR_INVARIANT, "the host log cannot reach training step %lld (no snapshot <= it "
+                        "rolls forward over complete ring slots; newest usable %lld)", (long long)T, (long long)gap);
+        }
     }
     unsigned long long bad = 0;
     CU(cudaMemcpyAsync(&bad, c->d_bad, sizeof bad, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
-    *mismatch = bad == ~0ull ? -1 : (int64_t)bad;
-    if (bad != ~0ull) return fail(c, CM_ERR_INVARIANT, "shadow != train at flat index %llu (step %lld)", bad, (long long)step);
-    return CM_OK;
+    if (bad == ~0ull) return CM_OK;
+    *mismatch = (int64_t)(bad >> 2);
+    const int w = (int)(bad & 3);
+    if (what) *what = w;
+    static const char* names[4] = {"p", "m", "v", "ring gradient"};
+    return fail(c, CM_ERR_INVARIANT, "checkpoint != training at flat index %llu (%s; step %lld, scope %d)",
+                bad >> 2, names[w], (long long)T, scope);
+}
+
+cm_status cm_verify(cm_ctx* c, int64_t* mismatch, void* stream) {
+    return cm_verify_ex(c, CM_VERIFY_SHADOW, mismatch, nullptr, stream);
 }
 
 // ---------------------------------------------------------------- restore
@@ -1902,6 +2049,7 @@ static bool slot_complete(const char* base, const SegHeader* h, int D, int nb, i
     const SlotMeta* meta = (const SlotMeta*)(base + h->meta_off);
     const volatile uint64_t* flags = (const volatile uint64_t*)(base + h->flags_off);
     const int slot = (int)((s - 1) % D);
+    if (h->nf_step >= 0 && s >= h->nf_step) return false;   // never roll forward to a non-finite step
     if (meta[slot].step_tag != s) return false;
     for (int bkt = 0; bkt < nb; ++bkt)
         if (flags[(size_t)slot * nb + bkt] != (uint64_t)s) return false;
@@ -1932,6 +2080,7 @@ static Reach reach_of(const SegHeader* h, const char* base, int D, int nb) {
     Reach r;
     for (int i = 0; i < 2; ++i) {
         r.snap[i] = h->half_step[i];
+        if (h->nf_step >= 0 && r.snap[i] >= h->nf_step) r.snap[i] = -1;   // conservative: at/after a flagged step
         if (r.snap[i] >= 0) r.lim[i] = roll_limit(base, h, D, nb, r.snap[i]);
     }
     return r;
@@ -1983,24 +2132,22 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
         for (int a = 0; a < 3; ++a)
             CU(cudaMemcpyAsync(c->sd[b & 1][a], c->sh[bi][a], (size_t)c->shard_numel * 4,
                                cudaMemcpyHostToDevice, s));
-        c->hh_step[0] = me.snap[0];
-        c->hh_step[1] = me.snap[1];
         // The roll-forward persists step I over the "older" half.  Never let that be the
         // source snapshot: a kill during the persist would leave this shard only a half
         // beyond I (this shard ran ahead of the consolidation point), and the next restore
-        // could not reach I.  A half beyond I is stale anyway (training recomputes it), so
-        // it is invalidated first and becomes the persist target; the source stays intact.
-        // (A half in (b, I] cannot exist: it would roll to I over a subset of the same ring
-        // slots, and pick() takes the newest such base.)
-        const int other = 1 - bi;
-        if (me.snap[other] > I) {
-            c->hdr->half_step[other] = -1;
-            c->hh_step[other] = -1;
+        // could not reach I.  A half beyond I is stale anyway (training recomputes it, maybe
+        // with other gradients), so it is invalidated first -- by its header step, also when
+        // reach_of() ignored it (at or after a non-finite step) -- and becomes the persist
+        // target; the source stays intact.  (A half in (b, I] cannot exist: it would roll to
+        // I over a subset of the same ring slots, and pick() takes the newest such base.)
+        for (int i = 0; i < 2; ++i) {
+            if (i != bi && c->hdr->half_step[i] > I) c->hdr->half_step[i] = -1;
+            c->hh_step[i] = i == bi ? b : (me.snap[i] > I ? -1 : me.snap[i]);
         }
     } else {
         // DEVICE placement: the HBM halves are the snapshots (half i holds step snap[i], i = step&1)
         for (int i = 0; i < 2; ++i)
-            if (me.snap[i] > I) c->hdr->half_step[i] = -1;   // training will recompute that step
+            if (c->hdr->half_step[i] > I) c->hdr->half_step[i] = -1;   // training will recompute that step
     }
     for (int64_t st = b + 1; st <= I; ++st) {   // roll forward over the ring
         const int slot = (int)((st - 1) % c->D);
@@ -2037,6 +2184,22 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     c->launches++;
     CHECK_LAUNCH();
     CU(cudaStreamSynchronize(s));
+    // Every rank has passed the all-gather's entry barrier, so every rank has computed I from
+    // the segment headers: only now may this rank's log change.  Steps beyond I are void
+    // (training recomputes them, possibly with different gradients): ring records and tap
+    // flags above I are invalidated, so a later restore can never roll forward over a slot
+    // that mixes the old run's and the new run's gradients.  The non-finite
+    // report is cleared: I precedes it.
+    for (int i = 0; i < c->D; ++i) {
+        SlotMeta* sm = slot_meta(c, i);
+        if (sm->step_tag > I) sm->step_tag = -1;
+        volatile uint64_t* fl = slot_flags(c, i);
+        for (size_t bk = 0; bk < c->buckets.size(); ++bk)
+            if (fl[bk] > (uint64_t)I) fl[bk] = 0;
+    }
+    c->hdr->nf_index = -1;
+    c->hdr->nf_step = -1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
     c->cur_iter = I;
     std::fill(c->issued.begin(), c->issued.end(), 0);
     c->issued_count = 0;
@@ -2049,6 +2212,60 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     c->stage_consumer[0] = c->stage_consumer[1] = false;
     for (int i = 0; i < c->D; ++i) c->slot_sc_step[i] = -1;
     *restored = I;
+    return CM_OK;
+}
+
+// CM_VERIFY_HOST: rebuild the training step T from the host segment alone -- the newest
+// host snapshot b <= T rolled forward over the tapped ring slots b+1..T with their recorded
+// scalars, exactly what cm_restore would do -- in chunks of the shadow staging size (scratch
+// p/m/v in HBM; the ring is read in place through its device alias), and compare every
+// chunk with the training state.  *gap_from >= 0 if no snapshot can reach T.
+static cm_status verify_host_log(cm_ctx* c, int64_t T, cudaStream_t s, int64_t* gap_from) {
+    *gap_from = -1;
+    const int nb = (int)c->buckets.size();
+    const Reach me = reach_of(c->hdr, c->seg, c->D, nb);
+    const int bi = me.pick(T);
+    if (bi < 0) {
+        *gap_from = me.hi();
+        return CM_OK;
+    }
+    const int64_t b = me.snap[bi];
+    cm_status st = ensure_staging(c);
+    if (st != CM_OK) return st;
+    const int64_t C = c->stg_elems;
+    if (!c->vf_scratch) CU(cudaMalloc(&c->vf_scratch, 3 * (size_t)C * 4));
+    float* sp = c->vf_scratch;
+    float* smm = sp + C;
+    float* sv = smm + C;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((C + 255) / 256, c->misc_blocks));
+    std::vector<StepRec> recs;
+    for (int64_t x = b + 1; x <= T; ++x) {
+        const SlotMeta* m = slot_meta(c, (int)((x - 1) % c->D));
+        float f[10];
+        for (int k = 0; k < 10; ++k) f[k] = m->sc[k];
+        recs.push_back(StepRec::from_floats(m->kind, f));
+    }
+    for (int64_t lo = 0; lo < c->shard_numel; lo += C) {
+        const int64_t len = std::min(C, c->shard_numel - lo);
+        CU(cudaMemcpyAsync(sp, c->sh[bi][0] + lo, (size_t)len * 4, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(smm, c->sh[bi][1] + lo, (size_t)len * 4, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(sv, c->sh[bi][2] + lo, (size_t)len * 4, cudaMemcpyHostToDevice, s));
+        for (int64_t x = b + 1; x <= T; ++x) {
+            AdamParams P{};
+            P.g = ring_slot_dev(c, (int)((x - 1) % c->D)) + lo * c->es;
+            P.n = len;
+            set_step(P, recs[x - b - 1]);
+            P.p_in = P.p_out = sp;
+            P.m_in = P.m_out = smm;
+            P.v_in = P.v_out = sv;
+            st = launch_adamw(c, P, c->shadow_blocks, s);
+            if (st != CM_OK) return st;
+        }
+        compare_kernel<<<grid, 256, 0, s>>>(sp, smm, sv, c->p, c->m, c->v, c->d_buckets, nb, c->n, c->rank, lo, len,
+                                            c->d_bad, c->zero1 ? 1 : 0);
+        c->launches++;
+        CHECK_LAUNCH();
+    }
     return CM_OK;
 }
 
@@ -2070,6 +2287,11 @@ cm_status cm_get_info(const cm_ctx* c, cm_info* o) {
     o->shadow_step = c->hdr ? c->hdr->shadow_step : -1;
     o->launches = c->launches;
     o->layout_hash = c->layout_hash;
+    o->nonfinite_step = c->nf_host ? c->nf_host[0] : -1;
+    o->nonfinite_index = c->nf_host ? c->nf_host[1] : -1;
+    o->persist_every = c->K;
+    o->host_half_step[0] = c->hdr ? c->hdr->half_step[0] : -1;
+    o->host_half_step[1] = c->hdr ? c->hdr->half_step[1] : -1;
     return CM_OK;
 }
 
@@ -2254,6 +2476,8 @@ cm_status cm_finalize(cm_ctx* c) {
     }
     if (c->d_done_ctr) cudaFree(c->d_done_ctr);
     if (c->d_bad) cudaFree(c->d_bad);
+    if (c->vf_scratch) cudaFree(c->vf_scratch);
+    if (c->ctl) cudaFreeHost(c->ctl);
     for (auto e : c->ev_tap_done) cudaEventDestroy(e);
     for (auto e : c->ev_gstep) if (e) cudaEventDestroy(e);
     for (auto e : c->ev_slot_free) cudaEventDestroy(e);

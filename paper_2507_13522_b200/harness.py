@@ -26,8 +26,12 @@ class Rank:
 
     def __init__(self, numel, world_size, rank, device, grad_dtype=cm.CM_F32, cap_bytes=W.CAP_BYTES,
                  shm_name="checkmate", ring_depth=2, shadow_place=cm.CM_SHADOW_HOST, flags=0,
-                 seed=W.SEED, init_state=True, persist_every=1):
+                 seed=W.SEED, init_state=True, persist_every=1, overwrite=True):
         self.numel = list(numel)
+        # the library refuses to replace a surviving shadow segment unless told to (it is the
+        # restore source after a hard kill); these drivers start fresh unless they attach
+        if overwrite and not flags & cm.CM_FLAG_ATTACH:
+            flags |= cm.CM_FLAG_OVERWRITE
         self.n, self.rank, self.device = world_size, rank, device
         self.grad_dtype, self.cap_bytes, self.seed = grad_dtype, cap_bytes, seed
         self.padded, self.n_buckets, self.tensor_off = cm.plan_buckets(self.numel, grad_dtype, cap_bytes,

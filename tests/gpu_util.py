@@ -59,3 +59,43 @@ def t2np(t):
 def bits(a):
     a = np.asarray(a)
     return a.view(np.uint32) if a.dtype == np.float32 else a
+
+
+def host_view(ptr, count, dtype):
+    """Zero-copy numpy view of host memory (a ring slot or a host snapshot half)."""
+    nbytes = count * np.dtype(dtype).itemsize
+    buf = (C.c_uint8 * nbytes).from_address(ptr)
+    return np.frombuffer(buf, dtype=dtype, count=count)
+
+
+def flat_to_local(rank_obj_list, flat_idx):
+    """flat indices -> (owner rank, shard-local index) arrays, from the library's bucket table."""
+    r0 = rank_obj_list[0]
+    n = r0.n
+    offs, pads = [], []
+    for b in range(r0.n_buckets):
+        off, padded, _ = r0.ctx.bucket_info(b)
+        offs.append(off)
+        pads.append(padded)
+    offs, pads = np.asarray(offs, np.int64), np.asarray(pads, np.int64)
+    flat_idx = np.asarray(flat_idx, np.int64)
+    b = np.searchsorted(offs, flat_idx, side="right") - 1
+    e = pads[b] // n
+    within = flat_idx - offs[b]
+    owner = within // e
+    local = offs[b] // n + within - owner * e
+    return owner, local
+
+
+def local_to_flat(rank_obj, local):
+    """shard-local index of rank_obj's shard -> flat index."""
+    for lo, hi, s in shard_slices(rank_obj):
+        if s <= local < s + (hi - lo):
+            return lo + (local - s)
+    raise IndexError(local)
+
+
+def flip_host_bit(ptr, index, dtype=np.uint32, bit=0):
+    """Flip one bit of element `index` of a host array in place (zero-copy)."""
+    a = host_view(ptr, index + 1, dtype)
+    a[index] ^= dtype(1 << bit)

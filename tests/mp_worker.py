@@ -119,7 +119,8 @@ def main():
         flags |= cm.CM_FLAG_TAP_DIRECT
     if mode.startswith("parity_nvls"):
         flags |= cm.CM_FLAG_NVLS
-    R = harness.DistRank(numel, dtype, cap, name, 2, cm.CM_SHADOW_HOST, flags, opt=opt)
+    # host shadow across processes: persist_every K >= 2 and ring depth D >= K + 1 (cm.h)
+    R = harness.DistRank(numel, dtype, cap, name, 3, cm.CM_SHADOW_HOST, flags, opt=opt, persist_every=2)
     if mode.startswith("parity_oneshot") or mode.startswith("parity_nvls") or mode == "parity_zero1_oneshot":
         # buckets up to 512 KiB / 1 MiB take the one-shot push kernel, the rest
         # the two-shot kernel; both must give the oracle's bits

@@ -2,7 +2,7 @@
 iterations, checkpointed vs the no-checkpoint NCCL baseline.
 
   python -m torch.distributed.run --nproc-per-node N tools/filler_mode.py \
-      [--tokens 16384] [--steps 6] [--warmup 2] [--ring-depth 8] [--persist-every 8]
+      [--tokens 16384] [--steps 6] [--warmup 2] [--ring-depth 9] [--persist-every 8]
 Rank 0 prints one JSON line.
 """
 import argparse
@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=16384, help="tokens per GPU per iteration")
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--ring-depth", type=int, default=8)
+    ap.add_argument("--ring-depth", type=int, default=9)
     ap.add_argument("--persist-every", type=int, default=8)
     ap.add_argument("--shadow", default="host", choices=["host", "device"])
     ap.add_argument("--arms", default="nccl,ours_nockpt,ours_ckpt")
