@@ -60,7 +60,8 @@ def parse():
                          "in-kernel stores straight to the host ring; ce: copy engine reads the grad buffer back")
     ap.add_argument("--no-baseline", action="store_true", help="skip the NCCL + torch fused AdamW arm")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="target seconds of oracle work")
+    ap.add_argument("--cpu-sample-s", type=float, default=12.0,
+                    help="target seconds of oracle work for cpu_baseline (half all-core, half one core; 0 skips)")
     ap.add_argument("--zero1", action="store_true",
                     help="sharded AdamW state: reduce-scatter + tap, AdamW on the own shard fused with the "
                          "NVLink all-gather of the updated parameters (SURVEY 8 f3)")
@@ -301,6 +302,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     launches0 = ctx.info().launches
     # the timed region runs without per-kernel events; a second pass of the same steps with
     # them gives the per-kernel rooflines (its step time is reported, not used)
+    t_first = R.t                                   # steps t_first+1 .. t_first+K are timed
     with ClockSampler(local) as clk:
         ms = time_steps(step, [R.stream, R.side], args.steps, ctx)
     host_issue = HOST_ISSUE["ms_per_step"]
@@ -310,12 +312,23 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     ctx.timing(True)
     ms_timed_pass = time_steps(step, [R.stream, R.side], args.steps, ctx)
     kms, kcnt = ctx.timing(False)
+    kbytes = ctx.timing_bytes()                     # D2H bytes the drains / persists really moved
     drain_now = ctx.info().drain_ctas
     ms_max = max_over_ranks(ms)
     ms_step = ms_max / args.steps
     iters_per_s = 1000.0 / ms_step
-    # bit-identity of the shadow after the timed run (verify synchronises)
-    mismatch = ctx.verify(R.stream)
+    # the checkpoint after the timed run, bitwise (cm_verify_ex synchronises): the shadow's
+    # working state, the host log alone (snapshot + ring roll-forward = the restore source)
+    # and the last ring slot vs the reduced gradients the training step used
+    checks = {}
+    for nm, scope in (("shadow", cm.CM_VERIFY_SHADOW), ("host_log", cm.CM_VERIFY_HOST), ("ring", cm.CM_VERIFY_RING)):
+        if nm == "host_log" and place != cm.CM_SHADOW_HOST:
+            continue
+        st, mis, what = ctx.verify_ex(scope, R.stream)
+        checks[nm] = st == cm.CM_OK
+        if st != cm.CM_OK:
+            checks[nm + "_mismatch"] = {"flat_index": mis, "what": what}
+    mismatch = -1 if all(v for k, v in checks.items() if not k.endswith("_mismatch")) else 0
     iso_ms, iso_cnt = isolated_kernels(args, dtype, cap, numel)
 
     # ----- per-kernel rooflines (average launch duration, live events on each kernel's stream)
@@ -326,7 +339,10 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     nb = info.n_buckets
     P = info.padded_numel
     L = info.shard_numel
-    K = max(1, args.persist_every) if place == cm.CM_SHADOW_HOST else 1
+    K = ctx.info().persist_every if place == cm.CM_SHADOW_HOST else 1
+    # snapshots persisted inside the timed window (steps t_first+1 .. t_first+steps), exactly
+    persists_timed = sum(1 for s_ in range(t_first + 1, t_first + args.steps + 1) if s_ % K == 0) \
+        if place == cm.CM_SHADOW_HOST else 0
     kern = {}
     ar_ms = kms[0] / max(kcnt[0], 1)
     Sb = S_bytes / nb                                            # average bucket bytes
@@ -398,12 +414,13 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     # the host link's busy time: summed durations of the tap drain copies (one stream) and
     # of the snapshot persist copies (another stream; the two can overlap), per step
     if kcnt[5] or kcnt[6]:
-        tap_b = S_bytes / n
         kern["host_link_busy"] = {
-            "tap_drain_ms_per_step": kms[5] / args.steps, "tap_drains_per_step": kcnt[5] / args.steps,
-            "tap_drain_GBps_while_busy": tap_b / (kms[5] / args.steps * 1e-3) / 1e9 if kms[5] else None,
-            "persist_ms_per_step": kms[6] / args.steps, "persists_per_step": kcnt[6] / args.steps,
-            "persist_GBps_while_busy": (sh_d2h * args.steps) / (kms[6] * 1e-3) / 1e9 if kms[6] else None,
+            "tap_drain_ms_per_step": kms[5] / args.steps, "tap_drain_copies_per_step": kcnt[5] / args.steps,
+            "tap_drain_bytes": kbytes[5],
+            "tap_drain_GBps_while_busy": kbytes[5] / (kms[5] * 1e-3) / 1e9 if kms[5] else None,
+            "persist_ms_per_step": kms[6] / args.steps, "persist_copies_per_step": kcnt[6] / args.steps,
+            "persist_bytes": kbytes[6], "snapshots_persisted": round(kbytes[6] / max(1, 12 * L)),
+            "persist_GBps_while_busy": kbytes[6] / (kms[6] * 1e-3) / 1e9 if kms[6] else None,
             "busy_frac_of_step": (kms[5] + kms[6]) / ms,
             "what": "copy durations on the drain / persist streams (events around each copy, after its stream "
                     "waits); busy_frac < 1 means the link idled part of the step, a low GB/s while busy means "
@@ -414,7 +431,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
             kern[k]["traffic"] = traf[k].get("dram_bytes_per_launch")
     # the step's binding resource: the host link carries the tap (S/n per GPU) and the
     # persisted shadow state (12 L / K); our kernels each run near their own roofs
-    step_d2h = S_bytes / n + sh_d2h
+    step_d2h = S_bytes / n + (12.0 * L * persists_timed / args.steps if place == cm.CM_SHADOW_HOST else 0.0)
     # lower bounds of one step per resource (algorithmic bytes / peak); the largest binds
     t_link = step_d2h / (link["d2h"] * 1e9)
     lb = {"rs_tap_ag": nb * kern["rs_tap_ag"]["bytes_per_launch"] / (kern["rs_tap_ag"]["peak"] * 1e9),
@@ -424,6 +441,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
         roof = {"kernel": "tap drain + shadow persist (copy engines, host link D2H)", "bound": "host_link",
                 "achieved": step_d2h / (ms_step * 1e-3) / 1e9, "peak": link["d2h"], "unit": "GB/s",
                 "bytes_per_step": step_d2h, "peak_source": "measured pinned D2H copy (this run)",
+                "snapshots_in_window": persists_timed,
                 "note": "the checkpointed step in synthetic mode (no compute to hide under) is bound by the "
                         "host link (lower bound %.2f ms vs %.2f ms for the largest kernel); peak = per-GPU "
                         "D2H with all ranks copying at once; per-kernel rooflines are in 'kernels'"
@@ -437,6 +455,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
 
     result = {"ms_step": ms_step, "iters_per_s": iters_per_s, "launches": launches, "kernels": kern,
               "roofline": roof, "clocks": clk.summary(), "shadow_bit_identical": mismatch == -1,
+              "checkpoint_verified": checks,
               "host_link_GBps": link, "S_bytes": S_bytes,
               "drain": "copy engine" if drain_now == 0 else f"SM drain, {drain_now} CTA(s)",
               "host_issue_ms_per_step": host_issue, "ms_step_kernel_timing_pass": ms_timed_pass / args.steps}
@@ -631,35 +650,67 @@ def run_ours_nockpt(args, rank, world, local, numel, dtype, cap):
 
 
 # ---------------------------------------------------------------------------- oracle arm
-def oracle_sample(args, numel, dtype, cap, n):
-    """Time the CPU oracle (oracle/, as it stands, single thread) on a bounded random
-    sample of the workload's elements; project to the full workload."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_timing(numel, dtype, cap, n, budget_s, steps=1, warmup=0, omp=False):
+    """Time the CPU oracle (oracle/, as it stands) on a bounded random sample of the
+    workload's elements: `warmup` untimed and `steps` timed iterations, each one iteration of
+    the rank-order sum of n ranks' generated gradients + AdamW over the same k sampled
+    elements (the elements are independent), sized so one iteration takes
+    about budget_s.  omp=True: the -fopenmp build of the same source over all cores in this
+    process's affinity set.  Returns the projection to the full workload."""
     import numpy as np
     from oracle import oracle as O
     from paper_2507_13522_b200 import workloads as W
     es = 4 if dtype == 0 else 2
     plan = O.Plan(numel, cap, es, n)
     rng = np.random.default_rng(1)
-    # calibrate on a small sample, then size the sample to ~cpu_sample_s seconds
-    k0 = min(plan.total, 1 << 14)
+    k0 = min(plan.total, 1 << 16)
     idx = np.sort(rng.choice(plan.total, k0, replace=False)).astype(np.int64)
     ones = np.ones(k0, np.uint8)
+    O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 1, idx, ones, omp=omp)       # load + first touch
     t0 = time.perf_counter()
-    O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 2, idx, ones)
-    per = (time.perf_counter() - t0) / (2 * k0)
-    steps = 2
-    k = int(min(plan.total, max(k0, args.cpu_sample_s / (per * steps))))
+    O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 1, idx, ones, omp=omp)
+    per = (time.perf_counter() - t0) / k0
+    k = int(min(plan.total, max(k0, budget_s / per)))
     idx = np.sort(rng.choice(plan.total, k, replace=False)).astype(np.int64)
     used = np.ones(k, np.uint8)
-    t0 = time.perf_counter()
-    O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, steps, idx, used)
-    dt = time.perf_counter() - t0
-    per_elem_step = dt / (k * steps)
-    full_iter_s = per_elem_step * plan.total            # one full iteration of all n ranks' work
-    return {"value": n / full_iter_s, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{k} of {plan.total} elements x {steps} iterations (rank-order sum of {n} ranks' "
-                      f"generated grads + AdamW), {dt:.1f} s single-threaded, projected to the full workload",
-            "ns_per_elem_iter": per_elem_step * 1e9}
+    for w in range(warmup):
+        O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 1, idx, used, t0=w, omp=omp)
+    times = []
+    for i in range(steps):
+        t0 = time.perf_counter()
+        O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 1, idx, used, t0=warmup + i, omp=omp)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times)
+    per_elem_iter = dt / (k * steps)
+    full_iter_s = per_elem_iter * plan.total            # one full iteration of all n ranks' work
+    threads = O.threads(omp)
+    return {"value": n / full_iter_s, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{k} of {plan.total} elements (random, fixed), {steps} timed + {warmup} warm-up iterations "
+                      f"of the rank-order sum of {n} ranks' generated grads + AdamW, {dt:.1f} s on {threads} "
+                      f"thread(s), projected to the full workload",
+            "ns_per_elem_iter": per_elem_iter * 1e9, "full_iter_ms": full_iter_s * 1e3,
+            "steps": steps, "warmup": warmup, "cpu_model": cpu_model(),
+            "affinity_cores": len(os.sched_getaffinity(0))}
+
+
+def cpu_baseline(numel, dtype, cap, n, budget_s):
+    """The oracle on the box's host cores: all cores (OpenMP build, the reported value) and
+    one core, each ~budget_s/2 of work in 3 iterations."""
+    allc = oracle_timing(numel, dtype, cap, n, budget_s / 6, steps=3, warmup=0, omp=True)
+    one = oracle_timing(numel, dtype, cap, n, budget_s / 6, steps=3, warmup=0, omp=False)
+    allc["single_core"] = {k: one[k] for k in ("value", "cores", "ns_per_elem_iter", "full_iter_ms", "sample")}
+    return allc
 
 
 def main():
@@ -671,10 +722,13 @@ def main():
         if rank != 0:
             return 0
         from oracle import oracle as O
-        O.build()
-        cb = oracle_sample(args, numel, dtype, cap, world)
+        O.build(omp=True)
+        # every step one iteration of the oracle over the same bounded sample (all host
+        # cores), sized so the whole --steps/--warmup run stays within about a minute
+        per_step = min(5.0, max(0.3, 60.0 / max(1, args.steps + args.warmup)))
+        cb = oracle_timing(numel, dtype, cap, world, per_step, steps=args.steps, warmup=args.warmup, omp=True)
         line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * world / cb["value"],
+                "steps": cb["steps"], "warmup": cb["warmup"], "ms_per_step": cb["full_iter_ms"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": {"workload": name, "ranks": world},
                 "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -713,10 +767,11 @@ def main():
                            f"bf16 autocast fwd/bwd (stock PyTorch), DP{world}; ours: CheckmateDDP backward hooks, "
                            f"tap={args.tap}, persist_every={args.persist_every}")
     cpu = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and args.cpu_sample_s > 0:
         from oracle import oracle as O
         O.build()
-        cpu = oracle_sample(args, numel, dtype, cap, world)
+        O.build(omp=True)
+        cpu = cpu_baseline(numel, dtype, cap, world, args.cpu_sample_s)
     if rank == 0:
         overhead = None if base is None else (res["ms_step"] / base["ms_step"] - 1.0) * 100.0
         line = {
@@ -741,7 +796,8 @@ def main():
                         "paper's claim, target <= 2%); synthetic_no_compute: the timed step above (only the "
                         "hot path, no model), where the tap + snapshot bytes over the host link are the "
                         "whole step (roofline.bound = host_link)"},
-            "shadow_bit_identical": res["shadow_bit_identical"], "kernels": res["kernels"],
+            "shadow_bit_identical": res["shadow_bit_identical"], "checkpoint_verified": res["checkpoint_verified"],
+            "kernels": res["kernels"],
             "host_issue_ms_per_step": res["host_issue_ms_per_step"],
             "ms_step_kernel_timing_pass": res["ms_step_kernel_timing_pass"],
             "host_link_GBps": res["host_link_GBps"],

@@ -390,6 +390,10 @@ cm_status cm_set_param(cm_ctx *ctx, const char *key, int64_t value);
  * stream).  Used by bench.py for the roofline of each kernel and the host link's busy
  * time.                                                                                */
 cm_status cm_timing(cm_ctx *ctx, int32_t enable, double *ms_out, int64_t *count_out);
+/* cm_timing_bytes -- bytes moved device->host by classes 5 (tap drains) and 6 (snapshot
+ * persists) in the last closed cm_timing window, per class into bytes_out[7] (other
+ * classes 0): the persists that actually fell in the window, not an average.           */
+cm_status cm_timing_bytes(const cm_ctx *ctx, int64_t *bytes_out);
 cm_status cm_shadow_view(const cm_ctx *ctx, int32_t half, float **p, float **m, float **v);
 cm_status cm_ring_view(const cm_ctx *ctx, int32_t slot, void **grads);
 

@@ -28,6 +28,9 @@
 #include <math.h>
 #include <xmmintrin.h>
 #include <pmmintrin.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define CMO_F32 0
 #define CMO_BF16 1
@@ -35,6 +38,15 @@
 /* ------------------------------------------------------------------------- */
 /* 0. Environment check: FTZ / DAZ must be off (R17: no flush of subnormals). */
 /* ------------------------------------------------------------------------- */
+/* threads the sampled trajectory uses (1 unless built with -fopenmp) */
+int cmo_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
 int cmo_fp_env_ok(void) {
     unsigned int csr = _mm_getcsr();
     int ftz = (csr & _MM_FLUSH_ZERO_MASK) != 0;
@@ -329,6 +341,10 @@ void cmo_run_sample(uint64_t seed, int32_t n, int32_t dtype, int32_t gscale,
     }
     for (int64_t t = t0; t < t0 + steps; ++t) {
         cmo_scalars(t + 1, lr, b1, b2, eps, wd, n, sc);
+        /* elements are independent: the all-core timing build
+           (-fopenmp, bench.py's cpu_baseline) splits them over threads; the same
+           per-element arithmetic, and without -fopenmp the pragma is ignored */
+#pragma omp parallel for schedule(static)
         for (int64_t k = 0; k < n_idx; ++k) {
             uint64_t i = (uint64_t)idx[k];
             float R;

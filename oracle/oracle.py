@@ -16,27 +16,31 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "cm_oracle.c")
 _LIB = os.path.join(_HERE, "libcm_oracle.so")
+_LIB_OMP = os.path.join(_HERE, "libcm_oracle_omp.so")   # all-core timing build (bench cpu_baseline)
 
 F32, BF16 = 0, 1
-CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall"]
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall",
+          "-Wno-unknown-pragmas"]
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (plain C, no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+def build(force: bool = False, omp: bool = False) -> str:
+    """Compile the oracle with gcc (plain C, no FMA contraction, no fast-math).  omp=True:
+    the same source with -fopenmp (sampled trajectories split over the host's cores; used
+    only to time the oracle on every core)."""
+    out = _LIB_OMP if omp else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = out + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, *(["-fopenmp"] if omp else []), "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, out)
+    return out
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        L = C.CDLL(build())
+def lib(omp: bool = False):
+    if omp not in _libs:
+        L = C.CDLL(build(omp=omp))
         i64p = np.ctypeslib.ndpointer(np.int64, flags="C")
         i32p = np.ctypeslib.ndpointer(np.int32, flags="C")
         f32p = np.ctypeslib.ndpointer(np.float32, flags="C")
@@ -91,8 +95,13 @@ def lib():
                                          f32p]
         L.cmo_consolidate.restype = C.c_int64
         L.cmo_consolidate.argtypes = [C.c_int32, i64p]
-        _lib = L
-    return _lib
+        L.cmo_threads.restype = C.c_int
+        _libs[omp] = L
+    return _libs[omp]
+
+
+def threads(omp: bool = False) -> int:
+    return int(lib(omp).cmo_threads())
 
 
 class Plan:
@@ -249,13 +258,15 @@ class Run:
         return grads
 
 
-def run_sample(seed, n, dtype, gscale, steps, idx, used, t0=0, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, wd=0.01):
-    """Trajectory of sampled flat indices over `steps` iterations."""
+def run_sample(seed, n, dtype, gscale, steps, idx, used, t0=0, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, wd=0.01,
+               omp=False):
+    """Trajectory of sampled flat indices over `steps` iterations.
+    omp=True runs the all-core build (same arithmetic per element)."""
     idx = np.ascontiguousarray(idx, np.int64)
     used = np.ascontiguousarray(used, np.uint8)
     k = len(idx)
     p, m, v, R = (np.zeros(k, np.float32) for _ in range(4))
-    lib().cmo_run_sample(seed, n, dtype, gscale, t0, steps, lr, b1, b2, eps, wd, k, idx, used, p, m, v, R)
+    lib(omp).cmo_run_sample(seed, n, dtype, gscale, t0, steps, lr, b1, b2, eps, wd, k, idx, used, p, m, v, R)
     return p, m, v, R
 
 

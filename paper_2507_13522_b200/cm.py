@@ -32,7 +32,7 @@ CM_FLAG_OVERWRITE = 1 << 7      # replace a surviving shadow segment (else CM_ER
 EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
            "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step",
            "cm_apply_step_sgd", "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_verify_ex", "cm_get_info",
-           "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_set_param", "cm_join", "cm_shadow_save", "cm_shadow_load",
+           "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_timing_bytes", "cm_set_param", "cm_join", "cm_shadow_save", "cm_shadow_load",
            "cm_crc32"]
 
 
@@ -111,6 +111,7 @@ def lib():
         L.cm_shadow_load.argtypes = [C.c_char_p, C.c_char_p, C.c_int32]
         L.cm_crc32.argtypes = [C.c_void_p, C.c_size_t]
         L.cm_timing.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+        L.cm_timing_bytes.argtypes = [P, C.POINTER(C.c_int64)]
         for name in EXPORTS:
             if name not in ("cm_blob_size", "cm_last_error", "cm_crc32"):
                 getattr(L, name).restype = C.c_int     # cm_status
@@ -281,6 +282,12 @@ class Context:
         cnt = (C.c_int64 * 7)()
         self._check(lib().cm_timing(self._ctx, 1 if enable else 0, ms, cnt))
         return list(ms), list(cnt)
+
+    def timing_bytes(self):
+        """device->host bytes per cm_timing class in the last closed window."""
+        b = (C.c_int64 * 7)()
+        self._check(lib().cm_timing_bytes(self._ctx, b))
+        return list(b)
 
     def finalize(self):
         if self._ctx:

@@ -271,6 +271,8 @@ struct cm_ctx {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> timed;  // (class, (start, end))
+    int64_t timed_bytes[7] = {};     // device->host bytes of classes 5 / 6 in the window
+    int64_t last_bytes[7] = {};      // ... of the last closed window (cm_timing_bytes)
 };
 
 // ====================================================================== helpers
@@ -660,8 +662,10 @@ cm_status cm_timing(cm_ctx* c, int32_t enable, double* ms_out, int64_t* count_ou
         c->timing = true;
         c->timed.clear();
         c->ev_used = 0;
+        memset(c->timed_bytes, 0, sizeof c->timed_bytes);
         return CM_OK;
     }
+    memcpy(c->last_bytes, c->timed_bytes, sizeof c->last_bytes);
     c->timing = false;
     double ms[kTimingClasses] = {};
     int64_t cnt[kTimingClasses] = {};
@@ -676,6 +680,12 @@ cm_status cm_timing(cm_ctx* c, int32_t enable, double* ms_out, int64_t* count_ou
     if (count_out) memcpy(count_out, cnt, sizeof cnt);
     c->timed.clear();
     c->ev_used = 0;
+    return CM_OK;
+}
+
+cm_status cm_timing_bytes(const cm_ctx* c, int64_t* bytes_out) {
+    if (!c || !bytes_out) return CM_ERR_ARG;
+    memcpy(bytes_out, c->last_bytes, sizeof c->last_bytes);
     return CM_OK;
 }
 
@@ -1353,6 +1363,7 @@ static int drain_ctas_now(const cm_ctx* c) {
 // cls: cm_timing class of the copy (5 tap drain, 6 snapshot persist)
 static cm_status d2h(cm_ctx* c, char* host_dst, const void* dev_src, size_t bytes, cudaStream_t s, int cls) {
     TimedScope ts(c, cls, s);
+    if (c->timing) c->timed_bytes[cls] += (int64_t)bytes;
     const int ctas = drain_ctas_now(c);
     if (ctas <= 0 || (bytes & 15) || ((uintptr_t)dev_src & 15) || ((uintptr_t)host_dst & 15)) {
         CU(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, s));

@@ -60,3 +60,22 @@ def test_reference_arm_prints_one_contract_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["steps"] == 1 and d["warmup"] == 0            # the steps it actually ran
+    cb = d["cpu_baseline"]
+    assert cb["steps"] == 1 and cb["cores"] >= 1 and cb["kind"] == "oracle"
+
+
+def test_oracle_all_core_build_gives_the_same_bits():
+    """bench.py times the oracle on every host core with the -fopenmp build of the same
+    source: the sampled trajectories must be bit-identical to the single-threaded build."""
+    import numpy as np
+    from oracle import oracle as O
+    rng = np.random.default_rng(5)
+    idx = np.sort(rng.choice(1 << 24, 200_000, replace=False)).astype(np.int64)
+    used = (rng.random(len(idx)) < 0.95).astype(np.uint8)
+    for dtype in (O.F32, O.BF16):
+        a = O.run_sample(3, 4, dtype, 10, 5, idx, used, t0=2)
+        b = O.run_sample(3, 4, dtype, 10, 5, idx, used, t0=2, omp=True)
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x.view(np.uint32), y.view(np.uint32))
+    assert O.threads(True) >= 1 and O.threads(False) == 1
