@@ -663,33 +663,34 @@ def cpu_model():
 
 def oracle_timing(numel, dtype, cap, n, budget_s, steps=1, warmup=0, omp=False):
     """Time the CPU oracle (oracle/, as it stands) on a bounded random sample of the
-    workload's elements: `warmup` untimed and `steps` timed iterations, each one iteration of
-    the rank-order sum of n ranks' generated gradients + AdamW over the same k sampled
-    elements (the elements are independent), sized so one iteration takes
-    about budget_s.  omp=True: the -fopenmp build of the same source over all cores in this
-    process's affinity set.  Returns the projection to the full workload."""
+    workload's elements: `warmup` untimed and `steps` timed iterations, each ONE iteration
+    of the rank-order sum of n ranks' generated gradients + AdamW over the same k sampled
+    elements, continuing their trajectories (the elements are independent,
+    PAPER.md:306-308), sized so one iteration takes about budget_s.  omp=True: the
+    -fopenmp build of the same source over all cores in this process's affinity set.
+    Returns the projection to the full workload."""
     import numpy as np
     from oracle import oracle as O
     from paper_2507_13522_b200 import workloads as W
     es = 4 if dtype == 0 else 2
     plan = O.Plan(numel, cap, es, n)
     rng = np.random.default_rng(1)
-    k0 = min(plan.total, 1 << 16)
+    k0 = min(plan.total, 1 << 18)
     idx = np.sort(rng.choice(plan.total, k0, replace=False)).astype(np.int64)
-    ones = np.ones(k0, np.uint8)
-    O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 1, idx, ones, omp=omp)       # load + first touch
+    cal = O.SampleRun(W.SEED, n, dtype, W.GRAD_SCALE, idx, np.ones(k0, np.uint8), omp=omp)
+    cal.iterate()                                          # load + first touch
     t0 = time.perf_counter()
-    O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 1, idx, ones, omp=omp)
+    cal.iterate()
     per = (time.perf_counter() - t0) / k0
     k = int(min(plan.total, max(k0, budget_s / per)))
     idx = np.sort(rng.choice(plan.total, k, replace=False)).astype(np.int64)
-    used = np.ones(k, np.uint8)
-    for w in range(warmup):
-        O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 1, idx, used, t0=w, omp=omp)
+    run = O.SampleRun(W.SEED, n, dtype, W.GRAD_SCALE, idx, np.ones(k, np.uint8), omp=omp)
+    for _ in range(warmup):
+        run.iterate()
     times = []
-    for i in range(steps):
+    for _ in range(steps):
         t0 = time.perf_counter()
-        O.run_sample(W.SEED, n, dtype, W.GRAD_SCALE, 1, idx, used, t0=warmup + i, omp=omp)
+        run.iterate()
         times.append(time.perf_counter() - t0)
     dt = sum(times)
     per_elem_iter = dt / (k * steps)

@@ -330,15 +330,22 @@ void cmo_iteration(int32_t n, int64_t total, int32_t dtype, const void *const *g
 /* Outputs p,m,v after `steps` steps and R of the last iteration (as float;    */
 /* for bf16 the bf16-rounded value).  Scalars use lr etc. constant over steps. */
 /* ------------------------------------------------------------------------- */
-void cmo_run_sample(uint64_t seed, int32_t n, int32_t dtype, int32_t gscale,
-                    int64_t t0, int64_t steps, double lr, double b1, double b2,
-                    double eps, double wd, int64_t n_idx, const int64_t *idx,
-                    const uint8_t *used, float *p, float *m, float *v, float *R_last) {
-    float sc[10];
+/* initial state of the sampled elements: p = p_0 (padding 0), m = v = 0 */
+void cmo_sample_init(uint64_t seed, int64_t n_idx, const int64_t *idx, const uint8_t *used,
+                     float *p, float *m, float *v, float *R_last) {
+#pragma omp parallel for schedule(static)
     for (int64_t k = 0; k < n_idx; ++k) {
         p[k] = used[k] ? cmo_gen_p0(seed, (uint64_t)idx[k]) : 0.0f;
         m[k] = 0.0f; v[k] = 0.0f; R_last[k] = 0.0f;
     }
+}
+
+/* iterations t0 .. t0+steps-1 of the sampled elements' trajectories (state in/out) */
+void cmo_sample_iterate(uint64_t seed, int32_t n, int32_t dtype, int32_t gscale,
+                        int64_t t0, int64_t steps, double lr, double b1, double b2,
+                        double eps, double wd, int64_t n_idx, const int64_t *idx,
+                        const uint8_t *used, float *p, float *m, float *v, float *R_last) {
+    float sc[10];
     for (int64_t t = t0; t < t0 + steps; ++t) {
         cmo_scalars(t + 1, lr, b1, b2, eps, wd, n, sc);
         /* elements are independent: the all-core timing build
@@ -363,6 +370,15 @@ void cmo_run_sample(uint64_t seed, int32_t n, int32_t dtype, int32_t gscale,
             R_last[k] = R;
         }
     }
+}
+
+void cmo_run_sample(uint64_t seed, int32_t n, int32_t dtype, int32_t gscale,
+                    int64_t t0, int64_t steps, double lr, double b1, double b2,
+                    double eps, double wd, int64_t n_idx, const int64_t *idx,
+                    const uint8_t *used, float *p, float *m, float *v, float *R_last) {
+    cmo_sample_init(seed, n_idx, idx, used, p, m, v, R_last);
+    cmo_sample_iterate(seed, n, dtype, gscale, t0, steps, lr, b1, b2, eps, wd, n_idx, idx, used,
+                       p, m, v, R_last);
 }
 
 /* ------------------------------------------------------------------------- */

@@ -83,6 +83,10 @@ def lib(omp: bool = False):
         L.cmo_run_sample.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
                                      C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                      C.c_int64, i64p, u8p, f32p, f32p, f32p, f32p]
+        L.cmo_sample_init.restype = None
+        L.cmo_sample_init.argtypes = [C.c_uint64, C.c_int64, i64p, u8p, f32p, f32p, f32p, f32p]
+        L.cmo_sample_iterate.restype = None
+        L.cmo_sample_iterate.argtypes = L.cmo_run_sample.argtypes
         L.cmo_sgd_scalars.restype = C.c_int
         L.cmo_sgd_scalars.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int32, f32p]
         L.cmo_sgd_f32.restype = None
@@ -268,6 +272,28 @@ def run_sample(seed, n, dtype, gscale, steps, idx, used, t0=0, lr=1e-3, b1=0.9, 
     p, m, v, R = (np.zeros(k, np.float32) for _ in range(4))
     lib(omp).cmo_run_sample(seed, n, dtype, gscale, t0, steps, lr, b1, b2, eps, wd, k, idx, used, p, m, v, R)
     return p, m, v, R
+
+
+class SampleRun:
+    """Sampled trajectories advanced one call at a time (state held here): bench.py times
+    single oracle iterations with it.  Same arithmetic as run_sample."""
+
+    def __init__(self, seed, n, dtype, gscale, idx, used, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, wd=0.01,
+                 omp=False):
+        self.idx = np.ascontiguousarray(idx, np.int64)
+        self.used = np.ascontiguousarray(used, np.uint8)
+        k = len(self.idx)
+        self.p, self.m, self.v, self.R = (np.zeros(k, np.float32) for _ in range(4))
+        self.args = (seed, n, dtype, gscale)
+        self.hp = (lr, b1, b2, eps, wd)
+        self.L = lib(omp)
+        self.t = 0
+        self.L.cmo_sample_init(seed, k, self.idx, self.used, self.p, self.m, self.v, self.R)
+
+    def iterate(self, steps=1):
+        self.L.cmo_sample_iterate(*self.args, self.t, steps, *self.hp, len(self.idx), self.idx, self.used,
+                                  self.p, self.m, self.v, self.R)
+        self.t += steps
 
 
 def run_sample_sgd(seed, n, dtype, gscale, steps, idx, used, t0=0, lr=1e-2, momentum=0.9, wd=0.0):

@@ -97,7 +97,14 @@ __device__ __forceinline__ bool nonfinite_f32(float x) { return (__float_as_uint
 __device__ __forceinline__ bool nonfinite_bf16(uint32_t h) { return (h & 0x7f80u) == 0x7f80u; }
 __device__ __noinline__ void nf_report(volatile int64_t* nf, int64_t step, int64_t index) {
     const int64_t cur = nf[0];
-    if (cur >= 0 && (cur < step || (cur == step && (index < 0 || nf[1] >= 0)))) return;
+    if (index < 0) {             // (the shadow: no flat index) never touches the index word
+        if (cur < 0 || cur > step) {
+            nf[0] = step;
+            __threadfence_system();
+        }
+        return;
+    }
+    if (cur >= 0 && (cur < step || (cur == step && nf[1] >= 0))) return;
     nf[1] = index;
     __threadfence_system();
     nf[0] = step;
