@@ -360,6 +360,16 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *   "lazy_exit"           1 (default): no exit barrier per bucket, the training step's
  *                         optimizer kernel starts with one iteration fence; 0: an exit
  *                         barrier per bucket (each all-reduce a complete collective)
+ *   "pdl"                 1: launch the all-reduce kernels with programmatic dependent launch
+ *                         (multi-process ranks): the next bucket's kernel launches and passes
+ *                         its entry barrier while the previous one still moves data.  It waits
+ *                         for its stream predecessor only when that was not one of this
+ *                         context's all-reduces, so the caller must not write gradients with
+ *                         its own kernels on the all-reduce stream between two calls (produce
+ *                         them on another stream + event, as a DDP comm stream does).  0
+ *                         (default): plain stream order
+ *   "ar_grid_switch_bytes" buckets up to this size take one block per SM instead of the
+ *                         co-resident cap (default 48 MiB; ignored once "ar_blocks" is set)
  *   "ar_impl"             0 (default) unrolled two-shot kernel, 1 software-pipelined variant
  *   "ar_pipe_blocks"      grid of ar_impl 1 (default 148, one block per SM)
  *   "zero1_impl"          ZeRO-1 AdamW + parameter all-gather kernel: 1 (default) two

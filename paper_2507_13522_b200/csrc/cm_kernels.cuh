@@ -52,6 +52,20 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
     return v;
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// The all-reduce kernels are launched with programmatic stream serialization (PDL): kernel
+// N+1 may start as soon as every block of kernel N has passed its entry barrier, so its launch
+// and its own entry barrier overlap kernel N's data phase.  Kernel N+1 touches only bucket
+// N+1 (disjoint from bucket N everywhere), so it needs no result of kernel N; it waits for
+// its predecessor (griddepcontrol.wait) only when that predecessor may have produced its
+// gradients (pdl_wait: the previous launch on the stream was not one of our all-reduces).
+// Every all-reduce kernel also waits for its predecessor before it EXITS, so kernels still
+// complete in stream order: an event or a normal launch after the last bucket's kernel
+// sees every earlier bucket's kernel complete, exactly as without PDL.  Both instructions
+// are no-ops for a launch without the PDL attribute.
+__device__ __forceinline__ void pdl_wait_prior() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_next() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ cross-GPU barrier
 // Pairwise flag exchange between block j of every rank (the grids of one collective
 // have equal size on all ranks).  pads[k] is rank k's signal pad (peer-mapped); slot
@@ -269,6 +283,8 @@ struct ArParams {
     volatile int64_t* nf;          // non-finite report (host-mapped step, index); nullptr: off
     int64_t elem0;                 // flat element index of the shard's first element
     int64_t nf_step;               // the step that applies this reduce (iteration + 1)
+    int pdl_wait;                  // 1: wait for the predecessor kernel (it may have written
+                                   // this bucket's gradients) before the entry barrier
 };
 
 // a reduced 16-byte vector (the value the tap and the all-gather store) is finite?  Else
@@ -367,7 +383,9 @@ __device__ __forceinline__ void ar_epilogue(const ArParams& P) {
 
 template <typename G, int N>
 __global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P) {
+    if (P.pdl_wait) pdl_wait_prior();
     if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 0);   // peers' grads are ready
+    pdl_launch_next();                                              // the next bucket may launch
 
     const int64_t stride = (int64_t)gridDim.x * kArThreads;
     int64_t q = blockIdx.x * (int64_t)kArThreads + threadIdx.x;
@@ -384,6 +402,7 @@ __global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P)
         ar_reduce_store<G, N>(P, q, x);
     }
     ar_epilogue<N>(P);
+    pdl_wait_prior();   // complete after the predecessor (stream-order completion)
 }
 
 // Software-pipelined variant (cm_set_param("ar_impl", 1)): one block per SM, each thread
@@ -392,7 +411,9 @@ __global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P)
 // of the links are busy at the same time instead of in alternating phases.
 template <typename G, int N>
 __global__ void __launch_bounds__(kArThreads, 1) rs_tap_ag_pipe_kernel(const ArParams P) {
+    if (P.pdl_wait) pdl_wait_prior();
     if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 0);   // peers' grads are ready
+    pdl_launch_next();
     const int64_t stride = (int64_t)gridDim.x * kArThreads;
     int64_t q = blockIdx.x * (int64_t)kArThreads + threadIdx.x;
     if (q < P.nvec) {
@@ -408,6 +429,7 @@ __global__ void __launch_bounds__(kArThreads, 1) rs_tap_ag_pipe_kernel(const ArP
         }
     }
     ar_epilogue<N>(P);
+    pdl_wait_prior();
 }
 
 // ------------------------------------------------------------------ one-shot push AR

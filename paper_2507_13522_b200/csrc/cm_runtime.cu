@@ -211,6 +211,12 @@ struct cm_ctx {
     int zero1_impl = 1;            // ZeRO-1 AdamW + AG: 1 two groups per thread in flight, 0 one,
                                    // 2 tiles pushed by bulk copies (cp.async.bulk)
     int ar_pipe_blocks = 148;
+    int ar_blocks_user = 0;        // ar_blocks set explicitly: no size-dependent grid
+    int64_t ar_grid_switch = 48ll << 20;   // buckets up to this many bytes: one block per SM
+    bool pdl = false;              // programmatic dependent launch of the all-reduce kernels
+    cudaStream_t last_s = nullptr; // stream of this context's latest launch on a caller stream,
+    int last_kind = 0;             // and its kind (1: an all-reduce kernel, 0: anything else)
+    int64_t last_iter = -1;        // iteration of that all-reduce kernel
     int tma_blocks = 148;
     int wt_blocks = 296;
     int wt1_blocks = 592;
@@ -436,18 +442,34 @@ static void launch_ar_pipe_t(int n, dim3 grid, cudaStream_t s, const ArParams& P
     }
 }
 
+// launch with programmatic stream serialization (PDL) when pdl is set (see cm_kernels.cuh)
+static cudaError_t launch_pdl(void (*k)(ArParams), dim3 grid, cudaStream_t s, bool pdl, const ArParams& P) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kArThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? at : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, P);
+}
+
 template <typename G>
-static void launch_ar_t(int n, dim3 grid, cudaStream_t s, const ArParams& P) {
+static void launch_ar_t(int n, dim3 grid, cudaStream_t s, const ArParams& P, bool pdl) {
+    void (*k)(ArParams) = nullptr;
     switch (n) {
-        case 1: rs_tap_ag_kernel<G, 1><<<grid, kArThreads, 0, s>>>(P); break;
-        case 2: rs_tap_ag_kernel<G, 2><<<grid, kArThreads, 0, s>>>(P); break;
-        case 3: rs_tap_ag_kernel<G, 3><<<grid, kArThreads, 0, s>>>(P); break;
-        case 4: rs_tap_ag_kernel<G, 4><<<grid, kArThreads, 0, s>>>(P); break;
-        case 5: rs_tap_ag_kernel<G, 5><<<grid, kArThreads, 0, s>>>(P); break;
-        case 6: rs_tap_ag_kernel<G, 6><<<grid, kArThreads, 0, s>>>(P); break;
-        case 7: rs_tap_ag_kernel<G, 7><<<grid, kArThreads, 0, s>>>(P); break;
-        default: rs_tap_ag_kernel<G, 8><<<grid, kArThreads, 0, s>>>(P); break;
+        case 1: k = rs_tap_ag_kernel<G, 1>; break;
+        case 2: k = rs_tap_ag_kernel<G, 2>; break;
+        case 3: k = rs_tap_ag_kernel<G, 3>; break;
+        case 4: k = rs_tap_ag_kernel<G, 4>; break;
+        case 5: k = rs_tap_ag_kernel<G, 5>; break;
+        case 6: k = rs_tap_ag_kernel<G, 6>; break;
+        case 7: k = rs_tap_ag_kernel<G, 7>; break;
+        default: k = rs_tap_ag_kernel<G, 8>; break;
     }
+    launch_pdl(k, grid, s, pdl, P);
 }
 
 template <typename G>
@@ -640,7 +662,9 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "ar_blocks_tap_only" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_tap_only = (int)value;
     else if (k == "shadow_blocks" && value >= 1 && value <= 65535) c->shadow_blocks = (int)value;
     else if (k == "tma_blocks" && value >= 1 && value <= 65535) c->tma_blocks = (int)value;
-    else if (k == "ar_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_blocks_max = (int)value;
+    else if (k == "ar_blocks" && value >= 1 && value <= kMaxBarrierBlocks) { c->ar_blocks_max = (int)value; c->ar_blocks_user = 1; }
+    else if (k == "ar_grid_switch_bytes" && value >= 0) c->ar_grid_switch = value;
+    else if (k == "pdl" && (value == 0 || value == 1)) c->pdl = value != 0;
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
     else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
@@ -1446,6 +1470,11 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     P.rank = c->rank;
     P.barriers = c->barriers ? 1 : 0;
     P.ag = (c->n > 1 && !c->zero1) ? 1 : 0;   // ZeRO-1 gathers the updated params instead
+    // PDL (multi-process ranks, cm_set_param "pdl"): wait for the predecessor only if it may
+    // have touched this bucket, i.e. unless the previous launch of this context on `s` was
+    // its all-reduce kernel of another bucket of the same iteration
+    const bool pdl = c->pdl && c->barriers;
+    P.pdl_wait = (pdl && c->last_s == s && c->last_kind == 1 && c->last_iter == t) ? 0 : 1;
     P.nf = c->nf_dev;                          // non-finite reduced values -> CM_ERR_INVARIANT
     P.elem0 = B.off + (int64_t)c->rank * shard;
     P.nf_step = t + 1;
@@ -1480,7 +1509,11 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     if (fused_tap) P.tap = ring_slot_dev(c, slot) + B.shard_off * c->es;
     else if (staged) P.tap = (char*)c->stage_buf[t & 1] + B.shard_off * c->es;
     const int64_t want = (P.nvec + (int64_t)kArThreads * kArUnroll - 1) / ((int64_t)kArThreads * kArUnroll);
-    const int cap_blocks = (c->n == 1 && fused_tap) ? std::min(c->ar_blocks_tap_only, c->ar_blocks_max) : c->ar_blocks_max;
+    // grid: buckets up to ar_grid_switch_bytes take one block per SM (leaves room for the next
+    // bucket's blocks to launch early under PDL; measured faster for 16-48 MiB, profiles/
+    // r01t_arblocks_*), larger ones the co-resident cap of the n-rank instance
+    int cap_blocks = (c->n == 1 && fused_tap) ? std::min(c->ar_blocks_tap_only, c->ar_blocks_max) : c->ar_blocks_max;
+    if (c->n > 1 && c->ar_blocks_user == 0 && B.padded * c->es <= c->ar_grid_switch) cap_blocks = std::min(cap_blocks, c->sms);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap_blocks));
     if (fused_tap) {
         P.done_ctr = c->d_done_ctr;
@@ -1546,11 +1579,16 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
             if (c->dtype == CM_F32) launch_ar_pipe_t<F32Tag>(c->n, pg, s, P);
             else launch_ar_pipe_t<BF16Tag>(c->n, pg, s, P);
         } else {
-            if (c->dtype == CM_F32) launch_ar_t<F32Tag>(c->n, grid, s, P);
-            else launch_ar_t<BF16Tag>(c->n, grid, s, P);
+            if (c->dtype == CM_F32) launch_ar_t<F32Tag>(c->n, grid, s, P, pdl);
+            else launch_ar_t<BF16Tag>(c->n, grid, s, P, pdl);
         }
         c->launches++;
         CHECK_LAUNCH();
+    }
+    if (!skip_kernel) {
+        c->last_s = s;
+        c->last_kind = 1;
+        c->last_iter = t;
     }
     if (!c->no_tap && (c->ce_tap || staged) && !c->ablate_no_drain) {
         // copy-engine drain of the reduced shard to the host ring, decoupled from the training
@@ -1734,6 +1772,8 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
         st = launch_adamw(c, P, c->adam_blocks, S(stream));
     }
     if (st != CM_OK) return st;
+    c->last_s = S(stream);
+    c->last_kind = 0;
     {   // the GPU step clock of the drain policy
         const int k = (int)(step % cm_ctx::kStepEv);
         if (!c->ev_gstep[k]) CU(cudaEventCreate(&c->ev_gstep[k]));
@@ -1889,6 +1929,8 @@ cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
                                        from_stage ? c->ev_stage_consumed[h] : nullptr);
     if (st != CM_OK) return st;
     if (from_stage) c->stage_consumer[h] = true;
+    c->last_s = s;
+    c->last_kind = 0;
     // release ring slots: DEVICE placement once consumed; HOST placement once a persisted
     // snapshot covers them (the ring is the log that makes every step recoverable)
     if (c->shadow_place == CM_SHADOW_DEVICE || persisted) {
@@ -1919,6 +1961,8 @@ cm_status cm_gen_grads(cm_ctx* c, uint64_t seed, int64_t t, int32_t scale, void*
     else
         gen_grads_kernel<BF16Tag><<<grid, 256, 0, S(stream)>>>(c->grad, nvec, c->d_buckets, (int)c->buckets.size(), K, scale);
     c->launches++;
+    c->last_s = S(stream);
+    c->last_kind = 0;
     CHECK_LAUNCH();
     return CM_OK;
 }
@@ -1943,6 +1987,8 @@ cm_status cm_init_state(cm_ctx* c, uint64_t seed, void* stream) {
         CU(cudaMemsetAsync(c->v, 0, (size_t)c->shard_numel * 4, S(stream)));
     }
     c->launches++;
+    c->last_s = S(stream);
+    c->last_kind = 0;
     CHECK_LAUNCH();
     return CM_OK;
 }
@@ -2031,6 +2077,8 @@ cm_status cm_verify_ex(cm_ctx* c, int32_t scope, int64_t* mismatch, int32_t* wha
     unsigned long long bad = 0;
     CU(cudaMemcpyAsync(&bad, c->d_bad, sizeof bad, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    c->last_s = s;
+    c->last_kind = 0;
     if (bad == ~0ull) return CM_OK;
     *mismatch = (int64_t)(bad >> 2);
     const int w = (int)(bad & 3);
@@ -2211,6 +2259,8 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     c->hdr->nf_index = -1;
     c->hdr->nf_step = -1;
     std::atomic_thread_fence(std::memory_order_seq_cst);
+    c->last_s = s;
+    c->last_kind = 0;
     c->cur_iter = I;
     std::fill(c->issued.begin(), c->issued.end(), 0);
     c->issued_count = 0;

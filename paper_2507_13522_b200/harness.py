@@ -47,8 +47,12 @@ class Rank:
         self.ctx = cm.Context(world_size, rank, device, ring_depth, shadow_place, shm_name, flags, persist_every)
         self.blob = self.ctx.register_buckets(self.numel, grad_dtype, cap_bytes, self.grad.data_ptr(),
                                               self.p.data_ptr(), self.m.data_ptr(), self.v.data_ptr())
+        # these drivers never write gradients on the all-reduce stream between two calls
+        # (cm_gen_grads is the library's own launch; DDP hooks produce them on another stream)
+        self.ctx.set_param("pdl", 1)
         # A/B switches for tools (collective settings: every rank must use the same value)
-        for key in ("lazy_exit", "drain_ctas", "oneshot_max_bytes", "ar_impl", "ar_pipe_blocks", "drain_flush_bytes", "numa_node", "zero1_impl", "shadow_blocks"):
+        for key in ("lazy_exit", "drain_ctas", "oneshot_max_bytes", "ar_impl", "ar_pipe_blocks", "drain_flush_bytes",
+                    "numa_node", "zero1_impl", "shadow_blocks", "pdl", "ar_grid_switch_bytes", "ar_blocks"):
             val = os.environ.get("CM_" + key.upper())
             if val is not None:
                 self.ctx.set_param(key, int(val))

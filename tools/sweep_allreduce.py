@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--min-kib", type=int, default=0, help="start size in KiB (overrides --min-mib)")
     ap.add_argument("--max-kib", type=int, default=0, help="end size in KiB (overrides --max-mib)")
     ap.add_argument("--nvls", action="store_true", help="CM_FLAG_NVLS: one-shot push via multimem.st")
+    ap.add_argument("--tag", default="", help="free-form label copied into every output line")
     ap.add_argument("--burst", type=int, default=1,
                     help="launches per timed rep (back to back, as in a step); time = total / burst")
     ap.add_argument("--oneshot-max", type=int, default=-1,
@@ -96,7 +97,7 @@ def main():
         med = tt.item()
         if rank == 0:
             sec = med * 1e-3
-            print(json.dumps({"mode": args.mode + ("_nvls" if args.nvls else ""), "burst": args.burst, "ar_blocks": args.ar_blocks, "oneshot_max": args.oneshot_max, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
+            print(json.dumps({"tag": args.tag, "mode": args.mode + ("_nvls" if args.nvls else ""), "burst": args.burst, "ar_blocks": args.ar_blocks, "oneshot_max": args.oneshot_max, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
                               "dtype": args.dtype, "n": n, "bytes": S, "ms": med,
                               "p10_ms": sorted(times)[len(times) // 10], "p90_ms": sorted(times)[9 * len(times) // 10],
                               "algbw_GBps": S / sec / 1e9, "busbw_GBps": 2 * (n - 1) / n * S / sec / 1e9,
