@@ -253,6 +253,22 @@ cm_status cm_apply_step(cm_ctx *ctx, int64_t step, const cm_adamw *hp, void *str
  * cm_apply_step; works with CM_FLAG_ZERO1 (velocity shard-local).                    */
 cm_status cm_apply_step_sgd(cm_ctx *ctx, int64_t step, const cm_sgd *hp, void *stream);
 
+/* cm_apply_bucket -- the training step `step` for ONE bucket, as soon as that bucket's
+ * all-reduce is issued ("the backward pass overlaps gradient
+ * computation and synchronization"): the optimizer of the bucket's elements runs on
+ * `stream` right behind its all-reduce (typically the DDP communication stream), overlapping
+ * the rest of the backward pass instead of running after it.  Same element arithmetic and
+ * bits as cm_apply_step.  Multi-process ranks: the kernel starts with a per-bucket fence
+ * (every rank's all-reduce of the bucket finished).  ZeRO-1: this rank's shard of the
+ * bucket, fused with the parameter all-gather.  Every bucket of a step must use identical
+ * hyper-parameters; all ranks must call it for the same buckets in the same order (like the
+ * all-reduces).  cm_apply_step(step) then finishes the step: it applies the buckets not yet
+ * applied and records the step's scalars for the shadow.  CM_ERR_STATE: bucket not
+ * all-reduced in this iteration, applied twice, other hyper-parameters; CM_ERR_INVARIANT
+ * after a non-finite report.                                                            */
+cm_status cm_apply_bucket(cm_ctx *ctx, int32_t bucket, int64_t step, const cm_adamw *hp, void *stream);
+cm_status cm_apply_bucket_sgd(cm_ctx *ctx, int32_t bucket, int64_t step, const cm_sgd *hp, void *stream);
+
 /* cm_shadow_apply -- the shadow replica's step `step` (Listing 2, PAPER.md:290-298:
  * "buckets.recv(); optimizer.step()"), enqueued on `side_stream`, off the training
  * stream's critical path.  Waits (stream-ordered) until every tap of iteration step-1 is

@@ -30,7 +30,7 @@ CM_FLAG_OVERWRITE = 1 << 7      # replace a surviving shadow segment (else CM_ER
 
 # every symbol include/cm.h declares (tests check the library exports all of them)
 EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
-           "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step",
+           "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step", "cm_apply_bucket", "cm_apply_bucket_sgd",
            "cm_apply_step_sgd", "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_verify_ex", "cm_get_info",
            "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_timing_bytes", "cm_set_param", "cm_join", "cm_shadow_save", "cm_shadow_load",
            "cm_crc32"]
@@ -95,6 +95,8 @@ def lib():
         L.cm_allreduce_multicast.argtypes = [P, C.c_int32, C.c_int64, P]
         L.cm_apply_step.argtypes = [P, C.c_int64, C.POINTER(cm_adamw), P]
         L.cm_apply_step_sgd.argtypes = [P, C.c_int64, C.POINTER(cm_sgd), P]
+        L.cm_apply_bucket.argtypes = [P, C.c_int32, C.c_int64, C.POINTER(cm_adamw), P]
+        L.cm_apply_bucket_sgd.argtypes = [P, C.c_int32, C.c_int64, C.POINTER(cm_sgd), P]
         L.cm_shadow_apply.argtypes = [P, C.c_int64, P]
         L.cm_restore.argtypes = [P, C.POINTER(C.c_int64), P]
         L.cm_gen_grads.argtypes = [P, C.c_uint64, C.c_int64, C.c_int32, P]
@@ -216,6 +218,14 @@ class Context:
     def apply_step_sgd(self, step, lr=1e-2, momentum=0.9, weight_decay=0.0, stream=None):
         hp = cm_sgd(lr, momentum, weight_decay)
         self._check(lib().cm_apply_step_sgd(self._ctx, int(step), C.byref(hp), _stream_ptr(stream)))
+
+    def apply_bucket(self, bucket, step, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, stream=None):
+        hp = cm_adamw(lr, beta1, beta2, eps, weight_decay)
+        self._check(lib().cm_apply_bucket(self._ctx, int(bucket), int(step), C.byref(hp), _stream_ptr(stream)))
+
+    def apply_bucket_sgd(self, bucket, step, lr=1e-2, momentum=0.9, weight_decay=0.0, stream=None):
+        hp = cm_sgd(lr, momentum, weight_decay)
+        self._check(lib().cm_apply_bucket_sgd(self._ctx, int(bucket), int(step), C.byref(hp), _stream_ptr(stream)))
 
     def shadow_apply(self, step, stream=None):
         self._check(lib().cm_shadow_apply(self._ctx, int(step), _stream_ptr(stream)))

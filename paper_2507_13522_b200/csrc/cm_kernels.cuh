@@ -785,6 +785,9 @@ __global__ void __launch_bounds__(kAdamThreads) sgd_wt_kernel(const AdamParams P
     wt_body<G, kOptSgd>(P);
 }
 
+// the step's scalar record alone (a per-bucket step: the bucket kernels carry no record)
+__global__ void record_kernel(const AdamParams P) { write_record(P); }
+
 // ------------------------------------------------------------------ AdamW, TMA-staged
 // Same arithmetic as adamw_kernel; data movement by the bulk-copy engine (TMA, 1-D
 // cp.async.bulk): one elected thread streams tiles of g, p, m, v into a kTmaStages-deep
@@ -942,6 +945,8 @@ struct Zero1Params {
     int64_t step;
     int unroll2;                    // 1: two groups per thread in flight (default), 0: one
     volatile int64_t* nf;           // non-finite report (flat index)
+    int64_t j0;                     // first shard-local element (per-bucket step: the bucket's
+                                    // shard_off; g then points at shard-local element j0)
 };
 
 // shard-local index j -> flat index of rank P.rank's element (b: running bucket index, j
@@ -991,14 +996,16 @@ __device__ __forceinline__ void z1_compute_store(const Zero1Params& P, int64_t j
 // loads issued before either is reduced and stored): the kernel's NVLink egress is n-1
 // stores per group, and one group of loads per thread left the link under-fed.
 template <typename G, int N, int OPT = kOptAdamW>
-__global__ void __launch_bounds__(256) adamw_zero1_kernel(const Zero1Params P) {
+__global__ void __launch_bounds__(256) adamw_zero1_kernel(Zero1Params P) {
     int b = 0;
     const int64_t groups = P.L / 4;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // shard-local j = P.j0 + 4q; g is indexed relative to j0, m, v, p absolutely
+    P.g = (const char*)P.g - P.j0 * GT<G>::kBytes;
     if (P.unroll2) {
         for (; q + stride < groups; q += 2 * stride) {
-            const int64_t j0 = q * 4, j1 = (q + stride) * 4;
+            const int64_t j0 = P.j0 + q * 4, j1 = P.j0 + (q + stride) * 4;
             const int64_t f0 = z1_flat(P, j0, b), f1 = z1_flat(P, j1, b);
             float4 g0, p0, m0, v0 = {}, g1, p1, m1, v1 = {};
             z1_load<G, OPT>(P, j0, f0, g0, p0, m0, v0);
@@ -1008,7 +1015,7 @@ __global__ void __launch_bounds__(256) adamw_zero1_kernel(const Zero1Params P) {
         }
     }
     for (; q < groups; q += stride) {
-        const int64_t j = q * 4;
+        const int64_t j = P.j0 + q * 4;
         const int64_t f = z1_flat(P, j, b);
         float4 g, p, m, v = {};
         z1_load<G, OPT>(P, j, f, g, p, m, v);

@@ -240,6 +240,10 @@ struct cm_ctx {
     int64_t cur_iter = 0;
     std::vector<char> issued;
     int issued_count = 0;
+    // per-bucket optimizer steps (cm_apply_bucket) of the current iteration
+    std::vector<char> applied;
+    int applied_count = 0;
+    StepRec bucket_rec;                 // the step's scalars, fixed by its first bucket
     int64_t train_step = 0;
     int64_t shadow_enq = 0;
     int K = 1;                       // persist the host snapshot every K shadow steps
@@ -1193,6 +1197,8 @@ cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
     }
     c->issued.assign(c->buckets.size(), 0);
     c->issued_count = 0;
+    c->applied.assign(c->buckets.size(), 0);
+    c->applied_count = 0;
     c->cur_iter = 0;
     c->train_step = 0;
     c->shadow_enq = 0;
@@ -1434,6 +1440,8 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
             c->cur_iter = t;
             std::fill(c->issued.begin(), c->issued.end(), 0);
             c->issued_count = 0;
+            std::fill(c->applied.begin(), c->applied.end(), 0);
+            c->applied_count = 0;
         } else {
             return fail(c, CM_ERR_STATE, "iteration %lld out of order (current %lld, %d/%zu buckets issued)",
                         (long long)t, (long long)c->cur_iter, c->issued_count, c->buckets.size());
@@ -1710,7 +1718,103 @@ static void update_gpu_period(cm_ctx* c, int64_t step) {
     }
 }
 
+// The optimizer step of ONE bucket (f1, cm_apply_bucket): the same element arithmetic over
+// the bucket's elements (ZeRO-1: its shard, fused with the parameter all-gather), started by
+// a per-bucket fence (block j waits for block j of every rank, i.e. for every rank's
+// all-reduce kernel of this bucket to have finished: its all-gather stores landed here and
+// nobody reads this bucket of our gradients any more).  No scalar record (cm_apply_step
+// writes it once all buckets are done).
+static cm_status launch_bucket_opt(cm_ctx* c, int b, int64_t step, const StepRec& rec, cudaStream_t s) {
+    const BucketDev& B = c->buckets[b];
+    AdamParams P{};
+    set_step(P, rec);
+    P.step = step;
+    P.nf = c->nf_dev;
+    if (c->zero1) {
+        Zero1Params Z{};
+        Z.g = (const char*)c->stage_buf[(step - 1) & 1] + B.shard_off * c->es;
+        Z.j0 = B.shard_off;
+        Z.L = B.padded / c->n;
+        Z.m = c->m; Z.v = c->v;
+        for (int k = 0; k < c->n; ++k) Z.p[k] = c->peer_p[k];
+        Z.buckets = c->d_buckets;
+        Z.nb = (int)c->buckets.size();
+        Z.n = c->n; Z.rank = c->rank; Z.barriers = c->barriers ? 1 : 0;
+        Z.s = P.s;
+        Z.q = P.q;
+        Z.pads = c->pads;
+        Z.epoch = ++c->epoch;
+        Z.step = step;
+        Z.unroll2 = c->zero1_impl == 0 ? 0 : 1;
+        Z.nf = c->nf_dev;
+        Z.rec_kind = P.rec_kind;
+        const int64_t want = (Z.L / 4 + 255) / 256;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c->zero1_blocks));
+        TimedScope ts(c, 1, s);
+        if (Z.rec_kind == kOptSgd) {
+            if (c->dtype == CM_F32) launch_zero1_t<F32Tag, kOptSgd>(c->n, grid, s, Z);
+            else launch_zero1_t<BF16Tag, kOptSgd>(c->n, grid, s, Z);
+        } else {
+            if (c->dtype == CM_F32) launch_zero1_t<F32Tag, kOptAdamW>(c->n, grid, s, Z);
+            else launch_zero1_t<BF16Tag, kOptAdamW>(c->n, grid, s, Z);
+        }
+        c->launches++;
+        CHECK_LAUNCH();
+        return CM_OK;
+    }
+    P.g = (const char*)c->grad + B.off * c->es;
+    P.p_in = P.p_out = c->p + B.off;
+    P.m_in = P.m_out = c->m + B.off;
+    P.v_in = P.v_out = c->v + B.off;
+    P.n = B.padded;
+    P.nf_base = B.off;
+    if (c->barriers && c->n > 1) {
+        P.pads = c->pads;
+        P.epoch = ++c->epoch;
+        P.fence_n = c->n;
+        P.fence_rank = c->rank;
+    }
+    TimedScope ts(c, 1, s);
+    return launch_adamw(c, P, c->adam_blocks, s);
+}
+
+static bool same_rec(const StepRec& a, const StepRec& b) {
+    float fa[10], fb[10];
+    a.to_floats(fa);
+    b.to_floats(fb);
+    return a.kind == b.kind && memcmp(fa, fb, sizeof fa) == 0;
+}
+
+static cm_status apply_bucket_impl(cm_ctx* c, int32_t b, int64_t step, const StepRec& rec, void* stream) {
+    if (b < 0 || b >= (int32_t)c->buckets.size()) return fail(c, CM_ERR_ARG, "bucket %d out of range", b);
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
+    {
+        cm_status e = check_nf(c);
+        if (e != CM_OK) return e;
+    }
+    if (step != c->train_step + 1 || c->cur_iter != step - 1)
+        return fail(c, CM_ERR_STATE, "bucket step %lld: training is at step %lld, iteration %lld", (long long)step,
+                    (long long)c->train_step, (long long)c->cur_iter);
+    if (!c->issued[b]) return fail(c, CM_ERR_STATE, "bucket %d of iteration %lld not all-reduced yet", b, (long long)(step - 1));
+    if (c->applied[b]) return fail(c, CM_ERR_STATE, "bucket %d of step %lld applied twice", b, (long long)step);
+    if (c->opt_kind >= 0 && c->opt_kind != rec.kind) return fail(c, CM_ERR_STATE, "optimizer changed mid-run");
+    if (c->applied_count > 0 && !same_rec(rec, c->bucket_rec))
+        return fail(c, CM_ERR_STATE, "bucket %d of step %lld: hyper-parameters differ from the step's first bucket", b,
+                    (long long)step);
+    cm_status st = launch_bucket_opt(c, b, step, rec, S(stream));
+    if (st != CM_OK) return st;
+    c->bucket_rec = rec;
+    c->applied[b] = 1;
+    c->applied_count++;
+    c->last_s = S(stream);
+    c->last_kind = 0;
+    return CM_OK;
+}
+
 static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* stream) {
+    if (c->applied_count > 0 && !same_rec(rec, c->bucket_rec))
+        return fail(c, CM_ERR_STATE, "step %lld: hyper-parameters differ from its per-bucket steps", (long long)step);
     update_gpu_period(c, step);
     const int slot = (int)((step - 1) % c->D);
     c->slot_sc[slot] = rec;
@@ -1732,7 +1836,22 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
         P.step = step;
     }
     cm_status st;
-    if (c->zero1) {
+    if (c->applied_count > 0) {
+        // per-bucket steps already ran for some buckets (f1): the rest now, then the record
+        for (int b = 0; b < (int)c->buckets.size(); ++b) {
+            if (c->applied[b]) continue;
+            st = launch_bucket_opt(c, b, step, rec, S(stream));
+            if (st != CM_OK) return st;
+            c->applied[b] = 1;
+            c->applied_count++;
+        }
+        if (P.hp_rec) {
+            record_kernel<<<1, 1, 0, S(stream)>>>(P);
+            c->launches++;
+            CHECK_LAUNCH();
+        }
+        st = CM_OK;
+    } else if (c->zero1) {
         // ZeRO-1: AdamW on this rank's shard (reduced grads in staging half (step-1)&1),
         // fused with the NVLink all-gather of the updated parameters
         Zero1Params Z{};
@@ -1785,6 +1904,22 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
     c->train_step = step;
     c->opt_kind = rec.kind;
     return CM_OK;
+}
+
+cm_status cm_apply_bucket(cm_ctx* c, int32_t bucket, int64_t step, const cm_adamw* hp, void* stream) {
+    if (!c || !hp) return CM_ERR_ARG;
+    StepRec r;
+    r.kind = kOptAdamW;
+    r.a = make_scalars(c, step, *hp);
+    return apply_bucket_impl(c, bucket, step, r, stream);
+}
+
+cm_status cm_apply_bucket_sgd(cm_ctx* c, int32_t bucket, int64_t step, const cm_sgd* hp, void* stream) {
+    if (!c || !hp) return CM_ERR_ARG;
+    StepRec r;
+    r.kind = kOptSgd;
+    r.q = make_sgd_scalars(c, *hp);
+    return apply_bucket_impl(c, bucket, step, r, stream);
 }
 
 // Shadow step s on rank r's shard (shard-local arrays of L elements).  Chunks of
@@ -2263,6 +2398,8 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     c->last_kind = 0;
     c->cur_iter = I;
     std::fill(c->issued.begin(), c->issued.end(), 0);
+    std::fill(c->applied.begin(), c->applied.end(), 0);
+    c->applied_count = 0;
     c->issued_count = 0;
     c->train_step = I;
     c->shadow_enq = I;

@@ -9,6 +9,15 @@ step runs on a low-priority side stream (Listing 2).
 
 Plumbing only (tensor views, hooks, streams, events); every step of the path runs in the
 library's kernels.
+
+bucket_step=True (default): each bucket's optimizer step is launched right behind its
+all-reduce on the communication stream (cm_apply_bucket), so the optimizer overlaps the
+rest of the backward pass instead of running after it; step() then only finishes the step
+(scalar record for the shadow) and launches the shadow step.
+
+A GradProbe (optional) records, for sampled flat indices, every rank's gradients before the
+reduce and the state before the step, so a checker can recompute the reduce and the optimizer
+step of those elements with the oracle (SURVEY 8.d C2 model-mode parity).
 """
 from __future__ import annotations
 
@@ -23,7 +32,8 @@ from . import workloads as W
 class CheckmateDDP:
     def __init__(self, module: torch.nn.Module, device: int, world_size: int = 1, rank: int = 0,
                  cap_bytes: int = W.CAP_BYTES, shm_name: str = "cmddp", ring_depth: int = 16,
-                 persist_every: int = 8, shadow_place: int = cm.CM_SHADOW_HOST, flags: int = 0, hp=None):
+                 persist_every: int = 8, shadow_place: int = cm.CM_SHADOW_HOST, flags: int = 0, hp=None,
+                 bucket_step: bool = True):
         import torch.distributed as dist
         self.module = module
         self.params = [p for p in module.parameters() if p.requires_grad]
@@ -72,6 +82,8 @@ class CheckmateDDP:
         self.pending = list(self.size)
         self.t = 0
         self.issued = 0
+        self.bucket_step = bucket_step
+        self.probe = None
         for p in self.params:
             p.register_post_accumulate_grad_hook(self._hook)
 
@@ -79,23 +91,31 @@ class CheckmateDDP:
         b = self.bucket_of[p]
         self.pending[b] -= 1
         if self.pending[b] == 0:
+            if self.probe is not None:                         # (on the producing stream, before
+                self.probe.before_reduce(self, b)              # the event: nothing foreign on comm)
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(self.dev))     # this bucket's grads are written
             self.comm.wait_event(ev)
             self.r.ctx.allreduce_multicast(b, self.t, self.comm)
+            if self.bucket_step:
+                self.r.ctx.apply_bucket(b, self.t + 1, stream=self.comm, **self.hp)
             self.issued += 1
 
     def zero_grad(self):
         self.r.grad.zero_()
         self.pending = list(self.size)
         self.issued = 0
+        if self.probe is not None:
+            self.probe.before_step(self)
 
     def step(self):
         """After loss.backward(): wait for the all-reduces, AdamW, then the shadow step."""
         assert self.issued == len(self.size), "backward did not produce every bucket"
         cur = torch.cuda.current_stream(self.dev)
         cur.wait_stream(self.comm)
-        self.r.ctx.apply_step(self.t + 1, stream=cur, **self.hp)
+        self.r.ctx.apply_step(self.t + 1, stream=cur, **self.hp)   # (remaining buckets +) the step's record
+        if self.probe is not None:
+            self.probe.after_step(self)
         if not self.no_tap:
             self.r.ctx.shadow_apply(self.t + 1, self.side)
         self.t += 1
@@ -103,3 +123,36 @@ class CheckmateDDP:
     def finalize(self):
         torch.cuda.synchronize(self.dev)
         self.r.ctx.finalize()
+
+
+class GradProbe:
+    """Samples of one iteration for an external parity check (plumbing only: index copies).
+    idx: flat indices (sorted) into the registered buffers.  Per iteration it keeps this
+    rank's pre-reduce gradients, the pre-step p/m/v and the post-step R, p, m, v at idx."""
+
+    def __init__(self, ddp: CheckmateDDP, idx):
+        r = ddp.r
+        self.idx = torch.as_tensor(idx, dtype=torch.int64, device=r.p.device)
+        buckets = r.buckets()
+        self.sel = []
+        for off, padded, _ in buckets:
+            m = (self.idx >= off) & (self.idx < off + padded)
+            self.sel.append(torch.nonzero(m).flatten())
+        self.pre_grad = torch.zeros(len(self.idx), dtype=r.grad.dtype, device=r.p.device)
+        self.records = []
+
+    def before_step(self, ddp):
+        r = ddp.r
+        self.cur = {"step": ddp.t + 1, "p": r.p[self.idx].cpu(), "m": r.m[self.idx].cpu(), "v": r.v[self.idx].cpu()}
+
+    def before_reduce(self, ddp, b):
+        sel = self.sel[b]
+        if len(sel):
+            self.pre_grad[sel] = ddp.r.grad[self.idx[sel]]
+
+    def after_step(self, ddp):
+        r = ddp.r
+        torch.cuda.current_stream(r.p.device).synchronize()
+        self.cur.update(grad=self.pre_grad.cpu().clone(), R=r.grad[self.idx].cpu(), p_new=r.p[self.idx].cpu(),
+                        m_new=r.m[self.idx].cpu(), v_new=r.v[self.idx].cpu())
+        self.records.append(self.cur)

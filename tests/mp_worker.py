@@ -90,12 +90,57 @@ def llama_full_zero1(name):
     return R, int(mine.sum())
 
 
+def model_parity(name):
+    """SURVEY 8.d C2 model-mode parity at n > 1: GPT-2 small (stock PyTorch fwd/bwd, bf16
+    autocast, random tokens per rank) through CheckmateDDP with per-bucket optimizer steps;
+    every rank's pre-reduce gradients and pre-step state at sampled indices (+ bucket edges)
+    go to rank 0, which recomputes the rank-order reduce and AdamW with the oracle and
+    compares them with every rank's results bitwise; then the full checkpoint check."""
+    from paper_2507_13522_b200.ddp import CheckmateDDP, GradProbe
+    from paper_2507_13522_b200.modelbench import make_model
+    from tests.model_parity import check_records, probe_indices
+    n, rank = dist.get_world_size(), dist.get_rank()
+    local = int(os.environ["LOCAL_RANK"])
+    dev = torch.device("cuda", local)
+    model = make_model(0).to(dev)
+    model.train()
+    cd = CheckmateDDP(model, local, n, rank, shm_name=name, ring_depth=9, persist_every=8)
+    cd.probe = GradProbe(cd, probe_indices(cd, 1 << 14))
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    for _ in range(3):
+        tok = torch.randint(0, 50257, (2, 256), device=dev, generator=g)
+        cd.zero_grad()
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = model(tok, labels=tok).loss
+        loss.backward()
+        cd.step()
+    torch.cuda.synchronize()
+    st = cd.r.ctx.verify_ex(cm.CM_VERIFY_ALL, torch.cuda.current_stream())
+    assert st == (cm.CM_OK, -1, None), st
+    recs = [None] * n
+    dist.all_gather_object(recs, cd.probe.records)
+    if rank == 0:
+        out = check_records(recs, n, W.HP)
+        print(f"model parity: {out}", flush=True)
+    return cd
+
+
 def main():
     mode, name = sys.argv[1], sys.argv[2]
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = dist.get_world_size()
+    if mode == "model_parity":
+        cd = model_parity(name)
+        rk = dist.get_rank()
+        dist.barrier()
+        cd.finalize()
+        cm.unlink_shadow(name, rk)
+        dist.destroy_process_group()
+        print(f"rank {rk}: {mode} ok", flush=True)
+        return
     if mode == "llama_full_zero1":
         R, k = llama_full_zero1(name)
         dist.barrier()
@@ -113,7 +158,7 @@ def main():
         if opt == "sgd" else HP_O
     ref = O.Run(plan, seed=0, dtype=dtype, gscale=W.GRAD_SCALE, hp=hp_o, opt=opt)
     flags = cm.CM_FLAG_ATTACH if mode == "hardkill_phase2" else 0
-    if mode.startswith("parity_zero1"):
+    if mode.startswith("parity_zero1") or mode == "parity_bucket_step_zero1":
         flags |= cm.CM_FLAG_ZERO1
     if mode == "parity_oneshot_direct":
         flags |= cm.CM_FLAG_TAP_DIRECT
@@ -125,12 +170,71 @@ def main():
         # buckets up to 512 KiB / 1 MiB take the one-shot push kernel, the rest
         # the two-shot kernel; both must give the oracle's bits
         R.r.ctx.set_param("oneshot_max_bytes", (1 << 20) if "bf16" in mode else (512 << 10))
-    if mode.startswith("parity"):
+    if mode.startswith("parity_bucket_step"):
+        # f1: each bucket's optimizer step right behind its all-reduce (cm_apply_bucket), in
+        # reverse bucket order with the last two left to cm_apply_step
+        c = R.r.ctx
+        for t in range(6):
+            c.gen_grads(R.seed, R.t, R.gscale, R.stream)
+            for b in range(R.n_buckets):
+                c.allreduce_multicast(b, R.t, R.stream)
+            for b in reversed(range(2, R.n_buckets)):
+                c.apply_bucket(b, R.t + 1, stream=R.stream, **R.hp)
+            c.apply_step(R.t + 1, stream=R.stream, **R.hp)
+            c.shadow_apply(R.t + 1, R.side)
+            R.t += 1
+            ref.step()
+            R.sync()
+            check(R, ref, f"iteration {t}", plan if mode.endswith("zero1") else None)
+            st = c.verify_ex(cm.CM_VERIFY_ALL, R.stream)
+            assert st == (cm.CM_OK, -1, None), st
+    elif mode.startswith("parity"):
         for t in range(6):
             R.step()
             ref.step()
             R.sync()
             check(R, ref, f"iteration {t}", plan if mode.startswith("parity_zero1") else None)
+            st = R.r.ctx.verify_ex(cm.CM_VERIFY_ALL, R.stream)
+            assert st == (cm.CM_OK, -1, None), st
+    elif mode == "nonfinite":
+        # a NaN in rank n-1's gradients at an element of rank 0's shard, iteration 3: every
+        # rank reports it (CM_ERR_INVARIANT, flat index), no shadow applies step 4, restore
+        # returns 3 on every rank, and 3 more iterations match the oracle's clean run
+        for _ in range(3):
+            R.step()
+            ref.step()
+        R.sync()
+        off, padded, used = R.r.ctx.bucket_info(0)
+        i = off + min(used, padded // n) // 2
+        c = R.r.ctx
+        with torch.cuda.stream(R.stream):
+            torch.cuda._sleep(int(120e6))          # every call is issued before the kernels run
+        c.gen_grads(R.seed, R.t, R.gscale, R.stream)
+        if R.rank_id == n - 1:
+            with torch.cuda.stream(R.stream):
+                R.r.grad[i] = float("nan")
+        for b in range(R.n_buckets):
+            c.allreduce_multicast(b, R.t, R.stream)
+        c.apply_step(R.t + 1, stream=R.stream, **R.hp)
+        c.shadow_apply(R.t + 1, R.side)
+        R.t += 1
+        R.sync()
+        st = c.verify_ex(cm.CM_VERIFY_ALL, R.stream)
+        assert st == (cm.CM_ERR_INVARIANT, i, "nonfinite"), st
+        assert c.info().nonfinite_step == 4
+        if R.rank_id == 0:
+            assert c.info().shadow_step == 3
+        torch.cuda.synchronize()
+        dist.barrier()
+        I = c.restore(R.stream)
+        assert I == 3, I
+        assert c.info().nonfinite_step == -1
+        R.t = I
+        for _ in range(3):
+            R.step()
+            ref.step()
+        R.sync()
+        check(R, ref, "after non-finite restore")
     elif mode == "restore_soft":
         for _ in range(4):
             R.step()

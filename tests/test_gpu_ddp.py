@@ -23,12 +23,16 @@ def tiny_gpt2():
     return GPT2LMHeadModel(cfg)
 
 
-def test_checkmate_ddp_matches_oracle_adamw_on_model_gradients():
+@pytest.mark.parametrize("bucket_step", [False, True])
+def test_checkmate_ddp_matches_oracle_adamw_on_model_gradients(bucket_step):
+    """bucket_step=True: each bucket's AdamW runs on the comm stream right behind its
+    all-reduce, during backward (cm_apply_bucket); same bits."""
     from paper_2507_13522_b200.ddp import CheckmateDDP
     dev = torch.device("cuda", 0)
     model = tiny_gpt2().to(dev)
-    name = f"cmddpt{os.getpid()}"
-    cd = CheckmateDDP(model, 0, 1, 0, cap_bytes=64 << 10, shm_name=name, ring_depth=4, persist_every=2)
+    name = f"cmddpt{os.getpid()}_{int(bucket_step)}"
+    cd = CheckmateDDP(model, 0, 1, 0, cap_bytes=64 << 10, shm_name=name, ring_depth=4, persist_every=2,
+                      bucket_step=bucket_step)
     r = cd.r
     numel = [p.numel() for p in cd.params]
     assert len(cd.size) > 3                                # several buckets
@@ -53,11 +57,37 @@ def test_checkmate_ddp_matches_oracle_adamw_on_model_gradients():
             np.testing.assert_array_equal(r.p.cpu().numpy().view(np.uint32), p.view(np.uint32))
             np.testing.assert_array_equal(r.v.cpu().numpy().view(np.uint32), v.view(np.uint32))
             cd.side.synchronize()
-            assert r.ctx.verify(torch.cuda.current_stream()) == -1
+            assert r.ctx.verify_ex(cm.CM_VERIFY_ALL, torch.cuda.current_stream()) == (cm.CM_OK, -1, None)
         # the module's parameters are the flat buffer: a forward after the step sees p
         w = model.transformer.wte.weight
         off = r.tensor_off[0]
         assert w.data_ptr() == r.p[off:].data_ptr()
+    finally:
+        cd.finalize()
+        cm.unlink_shadow(name, 0)
+
+
+def test_grad_probe_model_parity_n1():
+    """The probe-based check used for n > 1 (tests/model_parity.py), here at n=1."""
+    from paper_2507_13522_b200.ddp import CheckmateDDP, GradProbe
+    from tests.model_parity import check_records, probe_indices
+    dev = torch.device("cuda", 0)
+    model = tiny_gpt2().to(dev)
+    name = f"cmddpp{os.getpid()}"
+    cd = CheckmateDDP(model, 0, 1, 0, cap_bytes=64 << 10, shm_name=name, ring_depth=4, persist_every=2)
+    cd.probe = GradProbe(cd, probe_indices(cd, 2048))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(6)
+    try:
+        for t in range(3):
+            tok = torch.randint(0, 1000, (4, 128), device=dev, generator=gen)
+            cd.zero_grad()
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                loss = model(tok, labels=tok).loss
+            loss.backward()
+            cd.step()
+        out = check_records([cd.probe.records], 1, W.HP)
+        assert out["iterations"] == 3 and out["elements"] >= 2048
     finally:
         cd.finalize()
         cm.unlink_shadow(name, 0)

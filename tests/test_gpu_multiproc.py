@@ -28,7 +28,8 @@ def counts():
 @pytest.mark.parametrize("mode", ["parity_f32", "parity_bf16", "parity_zero1", "parity_sgd",
                                   "parity_oneshot", "parity_oneshot_bf16", "parity_oneshot_direct",
                                   "parity_nvls", "parity_nvls_bf16", "parity_zero1_oneshot",
-                                  "restore_soft"])
+                                  "parity_bucket_step", "parity_bucket_step_zero1", "nonfinite",
+                                  "restore_soft", "model_parity"])
 def test_multiprocess(mode):
     for n in counts():
         name = f"cmmp{os.getpid()}_{mode}_{n}"
