@@ -26,6 +26,13 @@
  *   - Thread safety: one context is driven by one host thread at a time.
  *   - The library never falls back to a CPU implementation: without a usable CUDA
  *     device cm_init fails with CM_ERR_CUDA.
+ *   - Non-finite values ("non-finite input -> numeric error"; reading R16):
+ *     the all-reduce kernels check every reduced value and the optimizer kernels every
+ *     updated p/m/v.  An inf/NaN is reported into the segment header (step, flat index): the
+ *     shadow never applies or publishes that step, restore never rolls forward to it, and
+ *     every enqueueing call returns CM_ERR_INVARIANT (the report is read without
+ *     synchronising, so it surfaces at the first call after the flagging kernel ran;
+ *     cm_verify_ex always sees it) until cm_restore rolls back to the last finite step.
  */
 #ifndef CM_H_
 #define CM_H_
@@ -114,7 +121,11 @@ typedef struct {
                              every K steps (0/1 = every step).  Every step stays recoverable
                              from host memory alone: restore rolls forward over the tapped
                              gradients since the snapshot, so the host link carries 12/K
-                             instead of 12 B/element of state per step.  1 <= K <= D.     */
+                             instead of 12 B/element of state per step.  1 <= K <= D.
+                             Ranks in separate processes: K >= 2 (0/1 become 2) and
+                             D >= K + 1, else cm_connect fails with CM_ERR_CONFIG -- a hard
+                             kill can leave a peer's durable log up to two steps behind, and
+                             every shard must still reach that step.         */
     const char *shm_name; /* base name of the shadow segment; rank r uses "/<name>.r<r>".
                              Required unless CM_FLAG_NO_TAP.  Copied by cm_init.            */
     uint64_t flags;       /* CM_FLAG_*                                                      */
@@ -290,6 +301,15 @@ cm_status cm_shadow_apply(cm_ctx *ctx, int64_t step, void *side_stream);
  * that is NOT the roll-forward source (a half beyond I is invalidated first), so a kill
  * during restore leaves a segment from which the next cm_restore reaches I again.      */
 cm_status cm_restore(cm_ctx *ctx, int64_t *restored_step, void *stream);
+/* Preconditions and effects of cm_restore, beyond the above:
+ *   - every rank calls it after quiescing its own work (no kernel of the context in flight:
+ *     synchronise the device) and after a process-group barrier, so every rank reads the
+ *     same durable segment headers and computes the same I;
+ *   - it is the recovery from CM_ERR_INVARIANT (non-finite): I precedes the flagged step,
+ *     and the report is cleared;
+ *   - after every rank has computed I (the all-gather's entry barrier), this rank's log above
+ *     I is invalidated (ring records, tap flags, snapshot halves): those steps will be
+ *     recomputed, possibly with other gradients, and must never be rolled forward.        */
 
 /* ------------------------------------------------------------------ inputs / checks
  * cm_gen_grads -- synthetic gradients (gradient production) for this

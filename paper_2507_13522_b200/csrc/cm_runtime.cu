@@ -2618,9 +2618,30 @@ cm_status cm_shadow_load(const char* path, const char* shm_name, int32_t rank) {
     if (!f) return CM_ERR_ARG;
     FileHeader fh{};
     if (fread(&fh, sizeof fh, 1, f) != 1 || fh.magic != kFileMagic || fh.version != 1 || fh.rank != rank ||
-        fh.payload_bytes < sizeof(SegHeader)) {
+        fh.payload_bytes < sizeof(SegHeader) || fh.world_size < 1 || fh.world_size > kMaxRanks ||
+        fh.rank >= fh.world_size) {
         fclose(f);
         return CM_ERR_ARG;
+    }
+    // the payload size must be the file's (never trust the header to size a segment), and the
+    // segment header inside must describe the same segment before anything is created
+    {
+        struct stat fs;
+        if (fstat(fileno(f), &fs) != 0 || (uint64_t)fs.st_size != sizeof(FileHeader) + fh.payload_bytes) {
+            fclose(f);
+            return CM_ERR_ARG;
+        }
+        SegHeader sh{};
+        if (fread(&sh, sizeof sh, 1, f) != 1 || sh.magic != kMagic || sh.version != kVersion ||
+            sh.total != fh.payload_bytes || sh.rank != rank || sh.world_size != fh.world_size ||
+            sh.layout_hash != fh.layout_hash) {
+            fclose(f);
+            return CM_ERR_INVARIANT;
+        }
+        if (fseek(f, (long)sizeof fh, SEEK_SET) != 0) {
+            fclose(f);
+            return CM_ERR_ARG;
+        }
     }
     char name[256];
     snprintf(name, sizeof name, "/%s.r%d", shm_name, rank);

@@ -16,6 +16,7 @@ def _fake_segment(name, size, seed=0):
     rng = np.random.default_rng(seed)
     buf = bytearray(rng.integers(0, 256, size, dtype=np.uint8).tobytes())
     struct.pack_into("<Q", buf, 0, SEG_MAGIC)          # SegHeader.magic
+    struct.pack_into("<I", buf, 8, 2)                  # SegHeader.version
     struct.pack_into("<ii", buf, 12, 1, 0)             # world_size, rank
     struct.pack_into("<q", buf, 56, 7)                 # shadow_step
     struct.pack_into("<Q", buf, 48, 0x1234)            # layout_hash
@@ -56,6 +57,22 @@ def test_save_load_round_trip_and_corruption(tmp_path):
         assert not os.path.exists(f"/dev/shm/{name}y.r0")
         with pytest.raises(cm.CMError):
             cm.shadow_load(path, name + "z", 1)         # wrong rank
+        # a header that claims more payload than the file holds is refused before any
+        # segment is created (never size a segment from an untrusted header)
+        trunc = bytearray(raw[:-4096])
+        path.write_bytes(bytes(trunc))
+        with pytest.raises(cm.CMError) as e:
+            cm.shadow_load(path, name + "z", 0)
+        assert e.value.status == cm.CM_ERR_ARG
+        assert not os.path.exists(f"/dev/shm/{name}z.r0")
+        # a payload whose segment header describes another segment (total, layout)
+        other = bytearray(raw)
+        struct.pack_into("<Q", other, 64 + 112, len(payload) + 4096)
+        path.write_bytes(bytes(other))
+        with pytest.raises(cm.CMError) as e:
+            cm.shadow_load(path, name + "z", 0)
+        assert e.value.status == cm.CM_ERR_INVARIANT
+        assert not os.path.exists(f"/dev/shm/{name}z.r0")
     finally:
         for suffix in ("", "x", "y", "z"):
             try:

@@ -292,3 +292,27 @@ def test_c1_100_iterations_full_compare():
                 all_ok(g)
     finally:
         close(g)
+
+
+def test_surviving_segment_is_never_replaced_implicitly():
+    """a fresh context must not delete a surviving shadow segment (the restore
+    source after a hard kill).  Without CM_FLAG_OVERWRITE cm_connect refuses (CM_ERR_STATE);
+    CM_FLAG_ATTACH attaches; CM_FLAG_OVERWRITE starts fresh on purpose."""
+    numel = W.numels(W.c1())
+    g = group(numel, 1, D=2, K=1)
+    name = g._shm
+    try:
+        g.step()
+        close(g, unlink=False)
+        r = harness.Rank(numel, 1, 0, 0, cm.CM_F32, 1 << 20, name, 2, cm.CM_SHADOW_HOST, 0, overwrite=False)
+        with pytest.raises(cm.CMError) as e:
+            r.ctx.connect([r.blob])
+        assert e.value.status == cm.CM_ERR_STATE
+        r.ctx.finalize()
+        assert os.path.exists(f"/dev/shm/{name}.r0")
+        r2 = harness.Rank(numel, 1, 0, 0, cm.CM_F32, 1 << 20, name, 2, cm.CM_SHADOW_HOST, cm.CM_FLAG_ATTACH)
+        r2.ctx.connect([r2.blob])
+        assert r2.ctx.restore(None) == 1
+        r2.ctx.finalize()
+    finally:
+        cm.unlink_shadow(name, 0)
