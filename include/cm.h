@@ -169,6 +169,14 @@ cm_status cm_plan_buckets(const cm_layer_table *table, int32_t world_size,
                           int64_t *out_padded_numel, int32_t *out_n_buckets,
                           int64_t *tensor_elem_offset);
 
+/* cm_plan_bucket_table -- the same plan as a table: for bucket b its flat element offset
+ * off[b], padded length E_b = padded[b] and real elements used[b] (arrays of `capacity`
+ * entries, any may be NULL).  Rank r owns shard [off + r E_b/n, off + (r+1) E_b/n) of every
+ * bucket.  *out_n_buckets is always set; CM_ERR_ARG if capacity is too small.
+ * Host-only.                                                                            */
+cm_status cm_plan_bucket_table(const cm_layer_table *table, int32_t world_size, int32_t capacity, int64_t *off,
+                               int64_t *padded, int64_t *used, int32_t *out_n_buckets);
+
 /* ------------------------------------------------------------------ lifecycle
  * cm_init -- create a context for one rank: select the device, allocate the signal pad
  * used by the cross-GPU barriers.  CM_ERR_CONFIG for n outside 1..8, rank outside

@@ -29,7 +29,7 @@ CM_FLAG_NVLS = 1 << 6           # one-shot push through an NVLink-SHARP multicas
 CM_FLAG_OVERWRITE = 1 << 7      # replace a surviving shadow segment (else CM_ERR_STATE)
 
 # every symbol include/cm.h declares (tests check the library exports all of them)
-EXPORTS = ["cm_plan_buckets", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
+EXPORTS = ["cm_plan_buckets", "cm_plan_bucket_table", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
            "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step", "cm_apply_bucket", "cm_apply_bucket_sgd",
            "cm_apply_step_sgd", "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_verify_ex", "cm_get_info",
            "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_timing_bytes", "cm_set_param", "cm_join", "cm_shadow_save", "cm_shadow_load",
@@ -83,6 +83,8 @@ def lib():
         P = C.c_void_p
         L.cm_plan_buckets.argtypes = [C.POINTER(cm_layer_table), C.c_int32, C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        L.cm_plan_bucket_table.argtypes = [C.POINTER(cm_layer_table), C.c_int32, C.c_int32, C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
         L.cm_init.argtypes = [C.POINTER(cm_config), C.POINTER(P)]
         L.cm_register_buckets.argtypes = [P, C.POINTER(cm_layer_table), P, P, P, P, P, C.POINTER(C.c_size_t)]
         L.cm_blob_size.restype = C.c_size_t
@@ -138,6 +140,18 @@ def plan_buckets(numel, grad_dtype, cap_bytes, world_size):
     if st != CM_OK:
         raise CMError(st, "cm_plan_buckets rejected the table")
     return tot.value, nb.value, list(offs[:len(numel)])
+
+
+def plan_bucket_table(numel, grad_dtype, cap_bytes, world_size):
+    """cm_plan_bucket_table -> list of (off, padded, used) per bucket (host-only)."""
+    t, keep = _layer_table(numel, grad_dtype, cap_bytes)
+    cap = max(len(numel), 1)
+    off, pad, used = (C.c_int64 * cap)(), (C.c_int64 * cap)(), (C.c_int64 * cap)()
+    nb = C.c_int32(0)
+    st = lib().cm_plan_bucket_table(C.byref(t), int(world_size), cap, off, pad, used, C.byref(nb))
+    if st != CM_OK:
+        raise CMError(st, "cm_plan_bucket_table rejected the table")
+    return [(off[b], pad[b], used[b]) for b in range(nb.value)]
 
 
 def unlink_shadow(name, rank):

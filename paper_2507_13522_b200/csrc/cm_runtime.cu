@@ -735,6 +735,24 @@ cm_status cm_plan_buckets(const cm_layer_table* t, int32_t world_size, int64_t* 
     return CM_OK;
 }
 
+cm_status cm_plan_bucket_table(const cm_layer_table* t, int32_t world_size, int32_t capacity, int64_t* off,
+                               int64_t* padded, int64_t* used, int32_t* out_n_buckets) {
+    if (!t || !t->numel || !out_n_buckets) return CM_ERR_ARG;
+    if (t->grad_dtype != CM_F32 && t->grad_dtype != CM_BF16) return CM_ERR_CONFIG;
+    if (world_size < 1 || world_size > kMaxRanks) return CM_ERR_CONFIG;
+    PlanOut po;
+    if (!plan(t->numel, t->n_tensors, t->cap_bytes, t->grad_dtype == CM_F32 ? 4 : 2, world_size, po))
+        return CM_ERR_CONFIG;
+    *out_n_buckets = (int32_t)po.buckets.size();
+    if ((int64_t)po.buckets.size() > (int64_t)capacity) return CM_ERR_ARG;
+    for (size_t b = 0; b < po.buckets.size(); ++b) {
+        if (off) off[b] = po.buckets[b].off;
+        if (padded) padded[b] = po.buckets[b].padded;
+        if (used) used[b] = po.buckets[b].used;
+    }
+    return CM_OK;
+}
+
 cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
     if (!cfg || !out) return CM_ERR_ARG;
     *out = nullptr;

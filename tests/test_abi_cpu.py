@@ -46,6 +46,10 @@ def test_plan_matches_oracle_random():
         ref = O.Plan(numel, cap, 4 if dt == 0 else 2, n)
         assert tot == ref.total and nb == ref.n_buckets
         assert offs == list(ref.tensor_off)
+        table = cm.plan_bucket_table(numel, dt, cap, n)
+        assert [t[0] for t in table] == list(ref.bucket_off)
+        assert [t[1] for t in table] == list(ref.bucket_padded)
+        assert [t[2] for t in table] == list(ref.bucket_used)
 
 
 def test_plan_paper_models():
