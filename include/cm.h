@@ -428,6 +428,9 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *                         -2 (default) the node of the GPU's PCIe root from sysfs, -1 the
  *                         kernel's first-touch default, k >= 0 node k; MPOL_PREFERRED, best
  *                         effort (cm_info.numa_node reports the outcome)
+ *   "persist_queue"       1: snapshot persists go on the tap-drain stream (drains and persists
+ *                         take the device->host link one at a time); 0 (default) their own
+ *                         low-priority stream
  *   "drain_flush_bytes"   a pending run of adjacent tap drains is issued at this size
  *                         (default 8 MiB, at most 64 MiB)
  *   "ablate_no_drain"     1: staged taps are never drained to the host ring (cost ablation;

@@ -214,6 +214,7 @@ struct cm_ctx {
     int ar_blocks_user = 0;        // ar_blocks set explicitly: no size-dependent grid
     int64_t ar_grid_switch = 48ll << 20;   // buckets up to this many bytes: one block per SM
     bool pdl = false;              // programmatic dependent launch of the all-reduce kernels
+    bool persist_on_tap = false;   // snapshot persists on the tap-drain stream (one D2H queue)
     cudaStream_t last_s = nullptr; // stream of this context's latest launch on a caller stream,
     int last_kind = 0;             // and its kind (1: an all-reduce kernel, 0: anything else)
     int64_t last_iter = -1;        // iteration of that all-reduce kernel
@@ -669,6 +670,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "ar_blocks" && value >= 1 && value <= kMaxBarrierBlocks) { c->ar_blocks_max = (int)value; c->ar_blocks_user = 1; }
     else if (k == "ar_grid_switch_bytes" && value >= 0) c->ar_grid_switch = value;
     else if (k == "pdl" && (value == 0 || value == 1)) c->pdl = value != 0;
+    else if (k == "persist_queue" && (value == 0 || value == 1)) c->persist_on_tap = value != 0;
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
     else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
@@ -1967,6 +1969,14 @@ static cm_status ensure_staging(cm_ctx* c) {
     return CM_OK;
 }
 
+// The queue of snapshot persists: their own low-priority stream (default), or with
+// "persist_queue" = 1 the tap-drain stream, so drains and persists take the device->host link
+// one at a time in issue order instead of splitting it.
+static cudaStream_t persist_q(cm_ctx* c) {
+    if (c->persist_on_tap && c->cs_tap) return c->cs_tap;
+    return c->cs_d2h;
+}
+
 // One shadow step; returns (via *persisted) whether a host snapshot was written.  HBM
 // half step&1 receives the new state.  HOST placement persists it to the older host half
 // when step % K == 0 (or when forced): the host then holds a snapshot plus the tapped
@@ -2025,11 +2035,12 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
             if (st != CM_OK) return st;
             CU(cudaEventRecord(c->ev_stg_free[j], c->cs_k));
             if (persist) {   // copy engine D2H of the new state chunk into the host snapshot half
-                CU(cudaStreamWaitEvent(c->cs_d2h, c->ev_stg_free[j], 0));
+                cudaStream_t pq = persist_q(c);
+                CU(cudaStreamWaitEvent(pq, c->ev_stg_free[j], 0));
                 // SGD leaves v untouched (all zero in every half): p and the velocity only
                 for (int k = 0; k < (rec.kind == kOptSgd ? 2 : 3); ++k)
                 {
-                    cm_status pst = d2h(c, (char*)(c->sh[ph][k] + lo), c->sd[hout][k] + lo, (size_t)len * 4, c->cs_d2h, 6);
+                    cm_status pst = d2h(c, (char*)(c->sh[ph][k] + lo), c->sd[hout][k] + lo, (size_t)len * 4, pq, 6);
                     if (pst != CM_OK) return pst;
                 }
             }
@@ -2040,7 +2051,7 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
         if (grads_consumed) CU(cudaEventRecord(grads_consumed, c->cs_k));
         CU(cudaStreamWaitEvent(s, c->ev_join, 0));
         if (persist) {
-            CU(cudaEventRecord(c->ev_join, c->cs_d2h));
+            CU(cudaEventRecord(c->ev_join, persist_q(c)));
             CU(cudaStreamWaitEvent(s, c->ev_join, 0));
         }
     }

@@ -49,8 +49,11 @@ def run_arm(arm, args, rank, world, local):
         if getattr(args, "zero1", False):
             flags |= cm.CM_FLAG_ZERO1
         name = f"cmmm_{os.environ.get('MASTER_PORT', '0')}_{arm}"
+        # per-bucket optimizer steps behind each bucket's all-reduce (default; CM_BUCKET_STEP=0:
+        # one optimizer kernel after backward, the A/B arm)
         cd = CheckmateDDP(model, local, world, rank, shm_name=name, ring_depth=args.ring_depth,
-                          persist_every=args.persist_every, flags=flags)
+                          persist_every=args.persist_every, flags=flags,
+                          bucket_step=os.environ.get("CM_BUCKET_STEP", "1") != "0")
         if getattr(args, "drain_ctas", -1) != -1:   # override the library's auto drain policy
             cd.r.ctx.set_param("drain_ctas", args.drain_ctas)
         if arm == "ours_tap_nodrain":               # cost decomposition: staging stores, no D2H
@@ -99,7 +102,7 @@ def run_arm(arm, args, rank, world, local):
 
         def cleanup():
             full = not (flags & (cm.CM_FLAG_NO_TAP | cm.CM_FLAG_NO_SHADOW))
-            ok = cd.r.ctx.verify(torch.cuda.current_stream()) == -1 if full else None
+            ok = cd.r.ctx.verify_ex(cm.CM_VERIFY_ALL, torch.cuda.current_stream())[0] == cm.CM_OK if full else None
             cd.finalize()
             cm.unlink_shadow(name, rank)
             return ok

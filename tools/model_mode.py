@@ -57,7 +57,8 @@ def main():
         res = {"mode": "model", "model": "GPT-2 small (124M), random init, random tokens", "n_gpus": world,
                "micro_batch": args.micro_batch, "seq_len": 1024, "autocast": "bf16", "persist_every":
                args.persist_every, "ring_depth": args.ring_depth, "tap": args.tap, "zero1": args.zero1,
-               "drain_ctas": args.drain_ctas, **out}
+               "drain_ctas": args.drain_ctas,
+               "env": {k: v for k, v in os.environ.items() if k.startswith("CM_")}, **out}
         if "nccl" in out and "ours_ckpt" in out:
             res["ckpt_overhead_pct_vs_nccl"] = (out["ours_ckpt"]["ms_per_iter"] / out["nccl"]["ms_per_iter"] - 1) * 100
         if "ours_nockpt" in out and "ours_ckpt" in out:
