@@ -441,7 +441,8 @@ cm_status cm_set_param(cm_ctx *ctx, const char *key, int64_t value);
  * stream around its launch (after any stream waits).  enable=1 clears and starts
  * collecting; enable=0 stops, synchronises the events and returns the summed
  * milliseconds and launch counts per class into ms_out[7] / count_out[7] (either may be
- * NULL): 0 all-reduce+tap kernel, 1 training AdamW, 2 shadow AdamW, 3 gradient
+ * NULL): 0 all-reduce+tap kernel, 1 training AdamW, 2 shadow AdamW kernel (on its own
+ * stream, after its waits), 3 gradient
  * generation, 4 restore copy, 5 tap drains (device->host copies or SM-drain launches of
  * the staged tap, on the drain stream), 6 snapshot persists (device->host, on the persist
  * stream).  Used by bench.py for the roofline of each kernel and the host link's busy

@@ -1999,7 +1999,6 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
     }
     const char* ring = ring_slot_host(c, slot);
     {
-        TimedScope ts(c, 2, s);
         CU(cudaEventRecord(c->ev_fork, s));
         CU(cudaStreamWaitEvent(c->cs_h2d, c->ev_fork, 0));
         CU(cudaStreamWaitEvent(c->cs_k, c->ev_fork, 0));
@@ -2031,7 +2030,11 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
             P.nf = c->nf_dev;       // the shadow checks its own results too (index unknown: -1)
             P.nf_base = -1;
             P.skip_nf = c->nf_dev;  // and never applies a flagged step
-            st = launch_adamw(c, P, c->shadow_blocks, c->cs_k);
+            {   // cm_timing class 2: the shadow's optimizer kernel itself, on its stream, after
+                // its waits (the step's other parts -- persists -- are class 6)
+                TimedScope ts(c, 2, c->cs_k);
+                st = launch_adamw(c, P, c->shadow_blocks, c->cs_k);
+            }
             if (st != CM_OK) return st;
             CU(cudaEventRecord(c->ev_stg_free[j], c->cs_k));
             if (persist) {   // copy engine D2H of the new state chunk into the host snapshot half
