@@ -20,11 +20,14 @@ ap.add_argument("--dtype", default="f32")
 ap.add_argument("--shadow", default="host")
 ap.add_argument("--opt", default="adamw", choices=["adamw", "sgd"])
 ap.add_argument("--drain-ctas", type=int, default=-1, help="force the SM drain (k CTAs) for profiling it")
+ap.add_argument("--ring-depth", type=int, default=2)
+ap.add_argument("--persist-every", type=int, default=1)
 a = ap.parse_args()
 dtype = cm.CM_F32 if a.dtype == "f32" else cm.CM_BF16
 name = f"cmprof{os.getpid()}"
-g = harness.VirtualGroup(W.numels(W.gpt2_small()), a.n, 0, dtype, W.CAP_BYTES, name, 2,
-                         cm.CM_SHADOW_HOST if a.shadow == "host" else cm.CM_SHADOW_DEVICE, opt=a.opt)
+g = harness.VirtualGroup(W.numels(W.gpt2_small()), a.n, 0, dtype, W.CAP_BYTES, name, a.ring_depth,
+                         cm.CM_SHADOW_HOST if a.shadow == "host" else cm.CM_SHADOW_DEVICE, opt=a.opt,
+                         persist_every=a.persist_every)
 if a.drain_ctas >= 0:
     for r in g.ranks:
         r.ctx.set_param("drain_ctas", a.drain_ctas)
