@@ -29,10 +29,12 @@
  *   - Non-finite values ("non-finite input -> numeric error"; reading R16):
  *     the all-reduce kernels check every reduced value and the optimizer kernels every
  *     updated p/m/v.  An inf/NaN is reported into the segment header (step, flat index): the
- *     shadow never applies or publishes that step, restore never rolls forward to it, and
- *     every enqueueing call returns CM_ERR_INVARIANT (the report is read without
- *     synchronising, so it surfaces at the first call after the flagging kernel ran;
- *     cm_verify_ex always sees it) until cm_restore rolls back to the last finite step.
+ *     shadow never applies or publishes that step and restore never rolls forward to it.
+ *     The error is CM_ERR_INVARIANT from cm_check (no synchronisation) and cm_verify_ex
+ *     (synchronising) until cm_restore rolls back to the last finite step.  Collective calls
+ *     do not refuse on it: ranks see the report at different times, and one rank refusing a
+ *     collective its peers issued would leave their kernels at a barrier.  Poll cm_check and
+ *     agree across ranks (like a loss scaler's found-inf) before calling cm_restore.
  */
 #ifndef CM_H_
 #define CM_H_
@@ -354,6 +356,12 @@ cm_status cm_verify(cm_ctx *ctx, int64_t *mismatch, void *stream);
 #define CM_VERIFY_HOST 2
 #define CM_VERIFY_RING 4
 cm_status cm_verify_ex(cm_ctx *ctx, int32_t scope, int64_t *mismatch, int32_t *what, void *stream);
+
+/* cm_check -- the non-finite report, without synchronising: CM_ERR_INVARIANT with *step =
+ * the first flagged step and *index = a flat element index of it (-1 unknown) once a
+ * kernel that already ran saw an inf/NaN; CM_OK with *step = -1 otherwise.  Either pointer
+ * may be NULL.  Cleared by cm_restore.                                                    */
+cm_status cm_check(cm_ctx *ctx, int64_t *step, int64_t *index);
 
 /* Introspection (host-only, cheap). */
 typedef struct {

@@ -192,8 +192,8 @@ struct cm_ctx {
     std::vector<std::pair<uint64_t, void*>> opened;  // (peer base key, mapped ptr)
     bool in_process = false, barriers = true;
     uint32_t epoch = 0;
-    unsigned long long* d_done_ctr = nullptr;
-    unsigned long long done_total = 0;
+    unsigned long long* d_done_ctr = nullptr;            // [n_buckets]: blocks finished (direct tap)
+    std::vector<unsigned long long> done_total;          // per bucket: cumulative launch blocks
     unsigned long long* d_bad = nullptr;
     // non-finite report pair (step, index): host view + device alias.  Points into the segment
     // header once connected with a tap (it then survives the process), else into `ctl`.
@@ -310,10 +310,14 @@ static cm_status fail(cm_ctx* c, cm_status s, const char* fmt, ...) {
 
 static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 
-// Sticky numeric error (reading R16): once a kernel reported a non-finite value, every
-// enqueueing call refuses with CM_ERR_INVARIANT until cm_restore rolls back to the last
-// finite step.  The report is read from host-mapped memory (no synchronisation), so it
-// surfaces at the first call after the flagging kernel ran; cm_verify always sees it.
+// The non-finite report (reading R16) as a status: CM_ERR_INVARIANT once a kernel reported
+// an inf/NaN, until cm_restore rolls back to the last finite step.  Read from host-mapped
+// memory, no synchronisation.  Collective calls never refuse because of it: ranks observe
+// the report at different times, and a rank that refused a collective its peers issued would
+// leave their kernels waiting at a barrier.  The device side makes the report safe instead
+// (the shadow never applies or publishes the flagged step; restore never rolls forward to
+// it); callers poll cm_check (and agree across ranks, as with a loss-scaler's found-inf) or
+// see it from cm_verify_ex.
 static cm_status check_nf(cm_ctx* c) {
     if (!c->nf_host) return CM_OK;
     const int64_t st = c->nf_host[0];
@@ -713,6 +717,15 @@ cm_status cm_timing(cm_ctx* c, int32_t enable, double* ms_out, int64_t* count_ou
     return CM_OK;
 }
 
+cm_status cm_check(cm_ctx* c, int64_t* step, int64_t* index) {
+    if (!c) return CM_ERR_ARG;
+    const int64_t st = c->nf_host ? c->nf_host[0] : -1;
+    const int64_t ix = c->nf_host ? c->nf_host[1] : -1;
+    if (step) *step = st;
+    if (index) *index = ix;
+    return st >= 0 ? check_nf(c) : CM_OK;
+}
+
 cm_status cm_timing_bytes(const cm_ctx* c, int64_t* bytes_out) {
     if (!c || !bytes_out) return CM_ERR_ARG;
     memcpy(bytes_out, c->last_bytes, sizeof c->last_bytes);
@@ -805,8 +818,7 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
     const size_t pad_bytes = (size_t)kPadRegions * kMaxBarrierBlocks * kMaxRanks * sizeof(uint32_t);
     CU(cudaMalloc(&c->pad, pad_bytes));
     CU(cudaMemset(c->pad, 0, pad_bytes));
-    CU(cudaMalloc(&c->d_done_ctr, sizeof(unsigned long long)));
-    CU(cudaMemset(c->d_done_ctr, 0, sizeof(unsigned long long)));
+
     CU(cudaMalloc(&c->d_bad, sizeof(unsigned long long)));
     CU(cudaHostAlloc((void**)&c->ctl, 64, cudaHostAllocMapped | cudaHostAllocPortable));
     c->ctl[0] = -1;
@@ -862,6 +874,11 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
     CU(cudaMalloc(&c->d_buckets, sizeof(BucketDev) * c->buckets.size()));
     CU(cudaMemcpy(c->d_buckets, c->buckets.data(), sizeof(BucketDev) * c->buckets.size(),
                   cudaMemcpyHostToDevice));
+    // direct tap: the last block of a bucket's launch publishes its flag.  One counter per
+    // bucket: launches of different buckets may overlap (PDL), launches of one bucket never do
+    CU(cudaMalloc(&c->d_done_ctr, sizeof(unsigned long long) * c->buckets.size()));
+    CU(cudaMemset(c->d_done_ctr, 0, sizeof(unsigned long long) * c->buckets.size()));
+    c->done_total.assign(c->buckets.size(), 0);
 
     // launch geometry (identical on every rank: same GPU model, same plan)
     int occ = c->dtype == CM_F32 ? ar_occupancy<F32Tag>(c->n) : ar_occupancy<BF16Tag>(c->n);
@@ -1450,10 +1467,6 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     if (c->cuda_dead) return CM_ERR_CUDA;
     if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
     if (bucket < 0 || bucket >= (int32_t)c->buckets.size()) return fail(c, CM_ERR_ARG, "bucket %d out of range", bucket);
-    {
-        cm_status e = check_nf(c);
-        if (e != CM_OK) return e;
-    }
     cudaStream_t s = S(stream);
     if (t != c->cur_iter) {
         if (t == c->cur_iter + 1 && c->issued_count == (int)c->buckets.size()) {
@@ -1544,9 +1557,9 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     if (c->n > 1 && c->ar_blocks_user == 0 && B.padded * c->es <= c->ar_grid_switch) cap_blocks = std::min(cap_blocks, c->sms);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap_blocks));
     if (fused_tap) {
-        P.done_ctr = c->d_done_ctr;
-        c->done_total += (unsigned long long)grid;
-        P.done_target = c->done_total;
+        P.done_ctr = c->d_done_ctr + bucket;
+        c->done_total[bucket] += (unsigned long long)grid;
+        P.done_target = c->done_total[bucket];
         P.tap_flag = to_dev(c, slot_flags(c, slot) + bucket);
         P.tap_flag_value = (uint64_t)(t + 1);
     }
@@ -1582,9 +1595,9 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         const int og = (int)std::max<int64_t>(1, std::min<int64_t>((O.nvec + kOsThreads - 1) / kOsThreads,
                                                                    kMaxBarrierBlocks));
         if (fused_tap) {
-            O.done_ctr = c->d_done_ctr;
-            c->done_total += (unsigned long long)og - (unsigned long long)grid;   // grid was counted above
-            O.done_target = c->done_total;
+            O.done_ctr = c->d_done_ctr + bucket;
+            c->done_total[bucket] += (unsigned long long)og - (unsigned long long)grid;   // grid was counted above
+            O.done_target = c->done_total[bucket];
             O.tap_flag = P.tap_flag;
             O.tap_flag_value = P.tap_flag_value;
         }
@@ -1601,8 +1614,8 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
             const int pg = (int)std::max<int64_t>(1, std::min<int64_t>(
                 (P.nvec + kArThreads - 1) / kArThreads, std::min(c->ar_pipe_blocks, c->sms)));
             if (fused_tap) {
-                c->done_total += (unsigned long long)pg - (unsigned long long)grid;
-                P.done_target = c->done_total;
+                c->done_total[bucket] += (unsigned long long)pg - (unsigned long long)grid;
+                P.done_target = c->done_total[bucket];
             }
             if (c->dtype == CM_F32) launch_ar_pipe_t<F32Tag>(c->n, pg, s, P);
             else launch_ar_pipe_t<BF16Tag>(c->n, pg, s, P);
@@ -1683,10 +1696,6 @@ static cm_status step_checks(cm_ctx* c, int64_t step, int kind) {
     if (c->cur_iter != step - 1 || c->issued_count != (int)c->buckets.size())
         return fail(c, CM_ERR_STATE, "step %lld before all buckets of iteration %lld were all-reduced (%d/%zu)",
                     (long long)step, (long long)(step - 1), c->issued_count, c->buckets.size());
-    {
-        cm_status e = check_nf(c);
-        if (e != CM_OK) return e;
-    }
     if (c->opt_kind >= 0 && c->opt_kind != kind)
         return fail(c, CM_ERR_STATE, "optimizer changed mid-run (%s after %s steps): m/v would change meaning",
                     kind == kOptSgd ? "SGD" : "AdamW", c->opt_kind == kOptSgd ? "SGD" : "AdamW");
@@ -1809,10 +1818,6 @@ static cm_status apply_bucket_impl(cm_ctx* c, int32_t b, int64_t step, const Ste
     if (b < 0 || b >= (int32_t)c->buckets.size()) return fail(c, CM_ERR_ARG, "bucket %d out of range", b);
     if (c->cuda_dead) return CM_ERR_CUDA;
     if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
-    {
-        cm_status e = check_nf(c);
-        if (e != CM_OK) return e;
-    }
     if (step != c->train_step + 1 || c->cur_iter != step - 1)
         return fail(c, CM_ERR_STATE, "bucket step %lld: training is at step %lld, iteration %lld", (long long)step,
                     (long long)c->train_step, (long long)c->cur_iter);
@@ -2072,10 +2077,6 @@ cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
     if (c->cuda_dead) return CM_ERR_CUDA;
     if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
     if (c->no_tap || c->no_shadow) return fail(c, CM_ERR_STATE, "context has no shadow (CM_FLAG_NO_TAP/NO_SHADOW)");
-    {
-        cm_status e = check_nf(c);
-        if (e != CM_OK) return e;
-    }
     if (step != c->shadow_enq + 1)
         return fail(c, CM_ERR_STATE, "shadow step %lld after %lld: iteration gap", (long long)step, (long long)c->shadow_enq);
     const int slot = (int)((step - 1) % c->D);

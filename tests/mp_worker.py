@@ -221,7 +221,7 @@ def main():
         R.sync()
         st = c.verify_ex(cm.CM_VERIFY_ALL, R.stream)
         assert st == (cm.CM_ERR_INVARIANT, i, "nonfinite"), st
-        assert c.info().nonfinite_step == 4
+        assert c.check() == (cm.CM_ERR_INVARIANT, 4, i)
         if R.rank_id == 0:
             assert c.info().shadow_step == 3
         torch.cuda.synchronize()
