@@ -632,6 +632,7 @@ def run_ours_nockpt(args, rank, world, local, numel, dtype, cap):
         # the step with two events around the all-reduce chain only: no event between two
         # all-reduce kernels, so the next bucket's kernel can launch early (PDL)
         c.gen_grads(R.seed, R.t, R.gscale, R.stream)
+        c.barrier(R.stream)                   # all ranks start the chain together (no skew in it)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(R.stream)
         for k in range(R.n_buckets):

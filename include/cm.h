@@ -357,6 +357,11 @@ cm_status cm_verify(cm_ctx *ctx, int64_t *mismatch, void *stream);
 #define CM_VERIFY_RING 4
 cm_status cm_verify_ex(cm_ctx *ctx, int32_t scope, int64_t *mismatch, int32_t *what, void *stream);
 
+/* cm_barrier -- a stream-ordered cross-GPU barrier (one tiny kernel; collective: every rank
+ * calls it in the same position of its call sequence).  Used to start timed regions of all
+ * ranks together (bench.py's lockstep all-reduce chain).  No-op for virtual ranks / n = 1.  */
+cm_status cm_barrier(cm_ctx *ctx, void *stream);
+
 /* cm_check -- the non-finite report, without synchronising: CM_ERR_INVARIANT with *step =
  * the first flagged step and *index = a flat element index of it (-1 unknown) once a
  * kernel that already ran saw an inf/NaN; CM_OK with *step = -1 otherwise.  Either pointer

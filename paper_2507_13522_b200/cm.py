@@ -31,7 +31,7 @@ CM_FLAG_OVERWRITE = 1 << 7      # replace a surviving shadow segment (else CM_ER
 # every symbol include/cm.h declares (tests check the library exports all of them)
 EXPORTS = ["cm_plan_buckets", "cm_plan_bucket_table", "cm_init", "cm_register_buckets", "cm_blob_size", "cm_connect",
            "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step", "cm_apply_bucket", "cm_apply_bucket_sgd",
-           "cm_apply_step_sgd", "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_verify_ex", "cm_check", "cm_get_info",
+           "cm_apply_step_sgd", "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_verify_ex", "cm_check", "cm_barrier", "cm_get_info",
            "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_timing_bytes", "cm_set_param", "cm_join", "cm_shadow_save", "cm_shadow_load",
            "cm_crc32"]
 
@@ -106,6 +106,7 @@ def lib():
         L.cm_verify.argtypes = [P, C.POINTER(C.c_int64), P]
         L.cm_verify_ex.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32), P]
         L.cm_check.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.cm_barrier.argtypes = [P, P]
         L.cm_get_info.argtypes = [P, C.POINTER(cm_info)]
         L.cm_bucket_info.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.cm_shadow_view.argtypes = [P, C.c_int32, C.POINTER(P), C.POINTER(P), C.POINTER(P)]
@@ -272,6 +273,9 @@ class Context:
         if st not in (CM_OK, CM_ERR_INVARIANT):
             self._check(st)
         return st, out.value, VERIFY_WHAT.get(what.value, what.value)
+
+    def barrier(self, stream=None):
+        self._check(lib().cm_barrier(self._ctx, _stream_ptr(stream)))
 
     def check(self):
         """cm_check -> (status, first flagged step or -1, flat index or -1); no synchronisation."""

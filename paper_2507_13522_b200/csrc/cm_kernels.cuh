@@ -785,6 +785,11 @@ __global__ void __launch_bounds__(kAdamThreads) sgd_wt_kernel(const AdamParams P
     wt_body<G, kOptSgd>(P);
 }
 
+// a bare cross-GPU barrier (cm_barrier): one block meets block 0 of every rank
+__global__ void barrier_kernel(const Pads pads, int n, int rank, uint32_t epoch) {
+    block_barrier(pads, n, rank, epoch, 0);
+}
+
 // the step's scalar record alone (a per-bucket step: the bucket kernels carry no record)
 __global__ void record_kernel(const AdamParams P) { write_record(P); }
 

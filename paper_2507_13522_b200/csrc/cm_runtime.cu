@@ -717,6 +717,19 @@ cm_status cm_timing(cm_ctx* c, int32_t enable, double* ms_out, int64_t* count_ou
     return CM_OK;
 }
 
+cm_status cm_barrier(cm_ctx* c, void* stream) {
+    if (!c) return CM_ERR_ARG;
+    if (c->cuda_dead) return CM_ERR_CUDA;
+    if (!c->connected) return fail(c, CM_ERR_STATE, "not connected");
+    if (!c->barriers || c->n == 1) return CM_OK;   // virtual ranks: one stream orders them already
+    barrier_kernel<<<1, 32, 0, S(stream)>>>(c->pads, c->n, c->rank, ++c->epoch);
+    c->launches++;
+    CHECK_LAUNCH();
+    c->last_s = S(stream);
+    c->last_kind = 0;
+    return CM_OK;
+}
+
 cm_status cm_check(cm_ctx* c, int64_t* step, int64_t* index) {
     if (!c) return CM_ERR_ARG;
     const int64_t st = c->nf_host ? c->nf_host[0] : -1;

@@ -67,6 +67,7 @@ def main():
     ev = []
     for _ in range(a.steps):
         c.gen_grads(R.seed, R.t, R.gscale, R.stream)
+        c.barrier(R.stream)
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(R.stream)
         for b in range(R.n_buckets):
