@@ -7,8 +7,11 @@ the oracle's uninterrupted trajectories, bit for bit.
   python -m torch.distributed.run --nproc-per-node N tools/restore_bench.py phase2kill <name> [k] [more] [delay_s]
   python -m torch.distributed.run --nproc-per-node N tools/restore_bench.py phase2 <name> [k] [more]
 Kill points of phase 1: "step" (after k whole iterations, their shadow
-and drain work still in flight), "after_ar" (k whole iterations, then iteration k's
-gradients and all-reduces + taps issued, the optimizer step never reached).  phase2kill
+and drain work still in flight), "before_rs" (k whole iterations, then iteration k's
+gradients produced, no all-reduce issued), "after_ar" (k whole iterations, then iteration
+k's gradients and all-reduces + taps issued, the optimizer step never reached),
+"mid_shadow" (k whole iterations with k a multiple of K = 8, killed 5 ms after the last
+one was issued: its shadow step and the persist of the 1.5 GB snapshot are in flight).  phase2kill
 attaches, starts cm_restore and SIGKILLs itself after delay_s (a kill mid-restore, possibly
 mid-persist of the rolled-forward snapshot); phase 2 must still restore.
 Rank 0 of phase 2 prints one JSON line (restore wall time, restored step, bit-exactness).
@@ -44,11 +47,15 @@ def main():
     if phase == "phase1":
         for _ in range(k):
             R.step()
-        if extra == "after_ar":
-            c = R.r.ctx
+        c = R.r.ctx
+        if extra in ("after_ar", "before_rs"):
             c.gen_grads(R.seed, R.t, R.gscale, R.stream)
-            for b in range(R.n_buckets):
-                c.allreduce_multicast(b, R.t, R.stream)
+            if extra == "after_ar":
+                for b in range(R.n_buckets):
+                    c.allreduce_multicast(b, R.t, R.stream)
+        if extra == "mid_shadow":
+            time.sleep(0.005)                 # the last shadow step + snapshot persist in flight
+            os._exit(0)
         # die with work still in flight (no stream sync, no finalize): whatever the GPUs did
         # not finish is lost; only the host shadow segments in /dev/shm survive
         dist.barrier()
@@ -75,7 +82,7 @@ def main():
     for _ in range(more):
         R.step()
     R.sync()
-    ok_shadow = R.r.ctx.verify(R.stream) == -1
+    ok_shadow = R.r.ctx.verify_ex(cm.CM_VERIFY_ALL, R.stream)[0] == cm.CM_OK
     # sampled bitwise comparison with the oracle's uninterrupted trajectories
     from oracle import oracle as O
     plan = O.Plan(numel, W.CAP_BYTES, 4, n)

@@ -20,7 +20,9 @@ one() {   # name k point [kill-delay]
   rm -f /dev/shm/$name.r*
 }
 one c5a$N 1 step
+one c5g$N 7 before_rs
 one c5b$N 7 after_ar
+one c5h$N 16 mid_shadow
 one c5c$N 50 step
 one c5d$N 11 step 0.005
 one c5e$N 11 step 0.03
