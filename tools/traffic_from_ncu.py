@@ -42,7 +42,7 @@ def main(path, out):
     # the last complete iteration: gen, 17 AR, train adamw, shadow adamw
     it = []
     for i in range(len(seq) - 1, -1, -1):
-        if seq[i][0].startswith("cm::gen_grads"):
+        if "gen_grads" in seq[i][0]:
             it = seq[i:i + 20]
             break
     ar = [m for nm, m in it if "rs_tap_ag" in nm]
