@@ -109,25 +109,34 @@ __device__ __forceinline__ void block_barrier(const Pads& pads, int n, int rank,
 // flat index from the all-reduce / training kernels preferred over an unknown one, -1).
 __device__ __forceinline__ bool nonfinite_f32(float x) { return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u; }
 __device__ __forceinline__ bool nonfinite_bf16(uint32_t h) { return (h & 0x7f80u) == 0x7f80u; }
-__device__ __noinline__ void nf_report(volatile int64_t* nf, int64_t step, int64_t index) {
-    const int64_t cur = nf[0];
+// The report lives twice: h, the host-mapped pair in the segment header (durable, read by
+// the host and by restore), and d, a device word holding the step (read by the shadow's
+// kernels: thousands of blocks reading one host-mapped word would serialise on PCIe).
+struct NfRef {
+    volatile int64_t* h;   // [step, index], host-mapped (nullptr: checks off)
+    volatile int64_t* d;   // [step], device memory
+};
+__device__ __noinline__ void nf_report(NfRef nf, int64_t step, int64_t index) {
+    const int64_t dc = nf.d[0];
+    if (dc < 0 || dc > step) nf.d[0] = step;
+    const int64_t cur = nf.h[0];
     if (index < 0) {             // (the shadow: no flat index) never touches the index word
         if (cur < 0 || cur > step) {
-            nf[0] = step;
+            nf.h[0] = step;
             __threadfence_system();
         }
         return;
     }
-    if (cur >= 0 && (cur < step || (cur == step && nf[1] >= 0))) return;
-    nf[1] = index;
+    if (cur >= 0 && (cur < step || (cur == step && nf.h[1] >= 0))) return;
+    nf.h[1] = index;
     __threadfence_system();
-    nf[0] = step;
+    nf.h[0] = step;
     __threadfence_system();
 }
 // updated state of 4 consecutive elements (index idx0..idx0+3; -1: unknown)
-__device__ __forceinline__ void nf_check4(volatile int64_t* nf, int64_t step, int64_t idx0, const float4& p,
+__device__ __forceinline__ void nf_check4(NfRef nf, int64_t step, int64_t idx0, const float4& p,
                                           const float4& m, const float4& v) {
-    if (!nf) return;
+    if (!nf.h) return;
     const float a[4] = {p.x, p.y, p.z, p.w}, b[4] = {m.x, m.y, m.z, m.w}, c[4] = {v.x, v.y, v.z, v.w};
     bool any = false;
 #pragma unroll
@@ -280,7 +289,7 @@ struct ArParams {
     unsigned long long done_target;
     volatile uint64_t* tap_flag;   // host-mapped (slot, bucket, rank) flag; nullptr: none
     uint64_t tap_flag_value;       // iteration + 1
-    volatile int64_t* nf;          // non-finite report (host-mapped step, index); nullptr: off
+    NfRef nf;                      // non-finite report (nf.h = nullptr: off)
     int64_t elem0;                 // flat element index of the shard's first element
     int64_t nf_step;               // the step that applies this reduce (iteration + 1)
     int pdl_wait;                  // 1: wait for the predecessor kernel (it may have written
@@ -290,8 +299,8 @@ struct ArParams {
 // a reduced 16-byte vector (the value the tap and the all-gather store) is finite?  Else
 // report the first non-finite element (flat index elem0 + q*V + k).
 template <typename G>
-__device__ __forceinline__ void nf_check_vec(volatile int64_t* nf, int64_t step, int64_t elem0, const uint4& r) {
-    if (!nf) return;
+__device__ __forceinline__ void nf_check_vec(NfRef nf, int64_t step, int64_t elem0, const uint4& r) {
+    if (!nf.h) return;
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
     if constexpr (std::is_same<G, F32Tag>::value) {
         bool any = false;
@@ -462,7 +471,7 @@ struct OsParams {
     unsigned long long done_target;
     volatile uint64_t* tap_flag;
     uint64_t tap_flag_value;
-    volatile int64_t* nf;          // non-finite report (see ArParams)
+    NfRef nf;                      // non-finite report (see ArParams)
     int64_t elem0;                 // flat element index of the bucket's first element
     int64_t nf_step;
 };
@@ -595,9 +604,10 @@ struct AdamParams {
     Pads pads;
     uint32_t epoch;
     int fence_n, fence_rank;       // fence_n = 0: no fence
-    volatile int64_t* nf;          // non-finite report of the updated state (nullptr: off)
+    NfRef nf;                      // non-finite report of the updated state (nf.h = nullptr: off)
     int64_t nf_base;               // flat index of element 0 of this launch (-1: not flat, e.g. shadow)
     const volatile int64_t* skip_nf;  // shadow: do nothing if the step (or an earlier) was flagged
+                                      // (the device word NfRef::d)
 };
 
 // whole-block early exit of a shadow kernel whose step was flagged non-finite (one host read
@@ -949,7 +959,7 @@ struct Zero1Params {
     int32_t rec_kind;
     int64_t step;
     int unroll2;                    // 1: two groups per thread in flight (default), 0: one
-    volatile int64_t* nf;           // non-finite report (flat index)
+    NfRef nf;                       // non-finite report (flat index)
     int64_t j0;                     // first shard-local element (per-bucket step: the bucket's
                                     // shard_off; g then points at shard-local element j0)
 };

@@ -199,7 +199,9 @@ struct cm_ctx {
     // header once connected with a tap (it then survives the process), else into `ctl`.
     int64_t* ctl = nullptr;               // pinned, mapped fallback pair
     volatile int64_t* nf_host = nullptr;
-    volatile int64_t* nf_dev = nullptr;
+    volatile int64_t* nf_dev = nullptr;   // device alias of nf_host (host-mapped)
+    int64_t* d_nf = nullptr;              // device word: the flagged step (read by shadow kernels)
+    NfRef nfref() const { return NfRef{nf_dev, (volatile int64_t*)d_nf}; }
     // cm_verify_ex scratch (chunked host roll-forward): p, m, v chunks
     float* vf_scratch = nullptr;
 
@@ -596,7 +598,7 @@ static cm_status publish(cm_ctx* c, volatile int64_t* host_field, int64_t value,
                          int64_t skip_step = -1) {
     // device alias of a header field
     volatile int64_t* d = (volatile int64_t*)(c->seg_dev + ((char*)host_field - c->seg));
-    publish_kernel<<<1, 1, 0, s>>>(d, value, skip_step >= 0 ? c->nf_dev : nullptr, skip_step);
+    publish_kernel<<<1, 1, 0, s>>>(d, value, skip_step >= 0 ? (const volatile int64_t*)c->d_nf : nullptr, skip_step);
     c->launches++;
     CHECK_LAUNCH();
     return CM_OK;
@@ -841,6 +843,11 @@ cm_status cm_init(const cm_config* cfg, cm_ctx** out) {
         int64_t* d = nullptr;
         CU(cudaHostGetDevicePointer((void**)&d, c->ctl, 0));
         c->nf_dev = d;
+    }
+    CU(cudaMalloc(&c->d_nf, sizeof(int64_t)));
+    {
+        const int64_t none = -1;
+        CU(cudaMemcpy(c->d_nf, &none, sizeof none, cudaMemcpyHostToDevice));
     }
     for (int i = 0; i < c->D; ++i) {
         cudaEvent_t a, b;
@@ -1379,6 +1386,10 @@ static cm_status create_or_attach_segment(cm_ctx* c) {
     CU(cudaHostGetDevicePointer((void**)&c->seg_dev, c->seg, 0));
     c->nf_host = &c->hdr->nf_step;    // the report now survives the process (restore reads it)
     c->nf_dev = to_dev(c, &c->hdr->nf_step);
+    {   // an attached segment may carry a previous run's report: the device word follows it
+        const int64_t st = c->hdr->nf_step;
+        CU(cudaMemcpy(c->d_nf, &st, sizeof st, cudaMemcpyHostToDevice));
+    }
     if (c->no_shadow) return CM_OK;   // tap-only benchmark mode: ring + flags, no replica
     if (c->shadow_place == CM_SHADOW_HOST) {
         float* base = (float*)(c->seg + c->hdr->state_off);
@@ -1529,7 +1540,7 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     // its all-reduce kernel of another bucket of the same iteration
     const bool pdl = c->pdl && c->barriers;
     P.pdl_wait = (pdl && c->last_s == s && c->last_kind == 1 && c->last_iter == t) ? 0 : 1;
-    P.nf = c->nf_dev;                          // non-finite reduced values -> CM_ERR_INVARIANT
+    P.nf = c->nfref();                          // non-finite reduced values -> CM_ERR_INVARIANT
     P.elem0 = B.off + (int64_t)c->rank * shard;
     P.nf_step = t + 1;
     // exit barrier only when the training step does not fence the iteration: ZeRO-1's
@@ -1602,7 +1613,7 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         O.pads = c->pads;
         O.epoch = P.epoch;
         O.rank = c->rank;
-        O.nf = c->nf_dev;
+        O.nf = c->nfref();
         O.elem0 = B.off;
         O.nf_step = t + 1;
         const int og = (int)std::max<int64_t>(1, std::min<int64_t>((O.nvec + kOsThreads - 1) / kOsThreads,
@@ -1771,7 +1782,7 @@ static cm_status launch_bucket_opt(cm_ctx* c, int b, int64_t step, const StepRec
     AdamParams P{};
     set_step(P, rec);
     P.step = step;
-    P.nf = c->nf_dev;
+    P.nf = c->nfref();
     if (c->zero1) {
         Zero1Params Z{};
         Z.g = (const char*)c->stage_buf[(step - 1) & 1] + B.shard_off * c->es;
@@ -1788,7 +1799,7 @@ static cm_status launch_bucket_opt(cm_ctx* c, int b, int64_t step, const StepRec
         Z.epoch = ++c->epoch;
         Z.step = step;
         Z.unroll2 = c->zero1_impl == 0 ? 0 : 1;
-        Z.nf = c->nf_dev;
+        Z.nf = c->nfref();
         Z.rec_kind = P.rec_kind;
         const int64_t want = (Z.L / 4 + 255) / 256;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c->zero1_blocks));
@@ -1864,7 +1875,7 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
     P.n = c->P_pad;
     set_step(P, rec);
     P.step = step;
-    P.nf = c->nf_dev;       // non-finite updated state -> CM_ERR_INVARIANT
+    P.nf = c->nfref();       // non-finite updated state -> CM_ERR_INVARIANT
     P.nf_base = 0;
     if (!c->no_tap) {
         SlotMeta* sm = slot_meta(c, slot);
@@ -1906,7 +1917,7 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
         Z.epoch = ++c->epoch;
         Z.hp_rec = P.hp_rec; Z.hp_kind = P.hp_kind; Z.hp_tag = P.hp_tag; Z.step = step;
         Z.unroll2 = c->zero1_impl;
-        Z.nf = c->nf_dev;
+        Z.nf = c->nfref();
         memcpy(Z.rec, P.rec, sizeof Z.rec);
         Z.rec_kind = P.rec_kind;
         const int64_t want = (Z.L / 4 + 255) / 256;
@@ -2045,9 +2056,9 @@ static cm_status shadow_step_enqueue(cm_ctx* c, int64_t step, const StepRec& rec
             P.p_in = c->sd[hin][0] + lo; P.m_in = c->sd[hin][1] + lo; P.v_in = c->sd[hin][2] + lo;
             P.p_out = c->sd[hout][0] + lo; P.m_out = c->sd[hout][1] + lo; P.v_out = c->sd[hout][2] + lo;
             P.step = step;
-            P.nf = c->nf_dev;       // the shadow checks its own results too (index unknown: -1)
+            P.nf = c->nfref();       // the shadow checks its own results too (index unknown: -1)
             P.nf_base = -1;
-            P.skip_nf = c->nf_dev;  // and never applies a flagged step
+            P.skip_nf = c->d_nf;    // and never applies a flagged step (device word)
             {   // cm_timing class 2: the shadow's optimizer kernel itself, on its stream, after
                 // its waits (the step's other parts -- persists -- are class 6)
                 TimedScope ts(c, 2, c->cs_k);
@@ -2440,6 +2451,10 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     c->hdr->nf_index = -1;
     c->hdr->nf_step = -1;
     std::atomic_thread_fence(std::memory_order_seq_cst);
+    {
+        const int64_t none = -1;
+        CU(cudaMemcpy(c->d_nf, &none, sizeof none, cudaMemcpyHostToDevice));
+    }
     c->last_s = s;
     c->last_kind = 0;
     c->cur_iter = I;
@@ -2743,6 +2758,7 @@ cm_status cm_finalize(cm_ctx* c) {
     if (c->d_bad) cudaFree(c->d_bad);
     if (c->vf_scratch) cudaFree(c->vf_scratch);
     if (c->ctl) cudaFreeHost(c->ctl);
+    if (c->d_nf) cudaFree(c->d_nf);
     for (auto e : c->ev_tap_done) cudaEventDestroy(e);
     for (auto e : c->ev_gstep) if (e) cudaEventDestroy(e);
     for (auto e : c->ev_slot_free) cudaEventDestroy(e);
