@@ -1189,21 +1189,33 @@ __global__ void __launch_bounds__(256) compare_kernel(const float* __restrict__ 
 
 // Bitwise compare of a tap ring slot (shard-local, read through its device alias) with the
 // reduced gradients the training step used: the flat grad buffer's shard r (ref_flat = 1) or
-// the shard-local staging half (ref_flat = 0, ZeRO-1).  Reports flat * 4 + 3.
+// the shard-local staging half (ref_flat = 0, ZeRO-1).  16-byte vectors (a shard is a whole
+// number of vectors and 16-byte aligned; the ring is read over PCIe, so the width matters).
+// Reports flat * 4 + 3 of the first differing element.
 __global__ void __launch_bounds__(256) compare_grads_kernel(const void* ring, const void* ref, int ref_flat,
                                                             const BucketDev* __restrict__ buckets, int nb, int n,
                                                             int rank, int64_t shard_n, int es,
                                                             unsigned long long* first_bad) {
+    const int per = 16 / es;                       // elements per vector
     int b = 0;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < shard_n;
-         j += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q * per < shard_n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = q * per;
         while (b + 1 < nb && j >= buckets[b + 1].shard_off) ++b;
         const BucketDev B = buckets[b];
         const int64_t flat = B.off + (int64_t)rank * (B.padded / n) + (j - B.shard_off);
         const int64_t ri = ref_flat ? flat : j;
-        const bool bad = es == 4 ? ((const volatile uint32_t*)ring)[j] != ((const uint32_t*)ref)[ri]
-                                 : ((const volatile uint16_t*)ring)[j] != ((const uint16_t*)ref)[ri];
-        if (bad) atomicMin(first_bad, (unsigned long long)flat * 4ull + 3ull);
+        const uint4 x = ld_cs_v4((const char*)ring + j * es);
+        const uint4 y = ld_v4((const char*)ref + ri * es);
+        if (x.x == y.x && x.y == y.y && x.z == y.z && x.w == y.w) continue;
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+        int k = 0;
+        for (int w = 0; w < 4; ++w) {
+            if (xs[w] == ys[w]) continue;
+            k = es == 4 ? w : 2 * w + (((xs[w] ^ ys[w]) & 0xFFFFu) ? 0 : 1);
+            break;
+        }
+        atomicMin(first_bad, (unsigned long long)(flat + k) * 4ull + 3ull);
     }
 }
 
