@@ -12,3 +12,7 @@ for mode in ours ours_tap nccl; do
   timeout 900 $RUN --master-port $port tools/sweep_allreduce.py --mode $mode --min-mib 1 --max-mib 1024 --reps 10 --burst 8 \
     --tag "r02 $mode" >> $F 2>> $OUT/${TAG}_sweep_n$N.err
 done
+# one iteration of 8 different buckets per timed rep (the in-step pattern: PDL overlap)
+port=$((port + 1))
+timeout 900 $RUN --master-port $port tools/sweep_allreduce.py --mode ours --multi-bucket --min-mib 1 --max-mib 512 \
+  --reps 10 --burst 8 --tag "r02 ours multi-bucket" >> $F 2>> $OUT/${TAG}_sweep_n$N.err

@@ -36,6 +36,9 @@ def main():
     ap.add_argument("--max-kib", type=int, default=0, help="end size in KiB (overrides --max-mib)")
     ap.add_argument("--nvls", action="store_true", help="CM_FLAG_NVLS: one-shot push via multimem.st")
     ap.add_argument("--tag", default="", help="free-form label copied into every output line")
+    ap.add_argument("--multi-bucket", action="store_true",
+                    help="ours: the burst is `burst` DIFFERENT buckets of one iteration (as in a training step: "
+                         "the next bucket's kernel may launch early, PDL) instead of one bucket over iterations")
     ap.add_argument("--burst", type=int, default=1,
                     help="launches per timed rep (back to back, as in a step); time = total / burst")
     ap.add_argument("--oneshot-max", type=int, default=-1,
@@ -53,7 +56,7 @@ def main():
     while kib <= kib_max:
         S = kib << 10
         mib = kib
-        numel = [S // es]
+        numel = [S // es] * (args.burst if args.multi_bucket and args.mode != "nccl" else 1)
         stream = torch.cuda.Stream(dev, priority=-1)
         if args.mode == "nccl":
             buf = torch.randn(S // es, device=dev).to(harness.TORCH_DT[dtype])
@@ -65,7 +68,7 @@ def main():
             name = f"cmsw_{os.environ.get('MASTER_PORT', '0')}_{mib}"
             if args.nvls:
                 flags |= cm.CM_FLAG_NVLS
-            R = harness.DistRank(numel, dtype, S + 1, name, 2, cm.CM_SHADOW_HOST, flags)
+            R = harness.DistRank(numel, dtype, S, name, 2, cm.CM_SHADOW_HOST, flags)
             if args.ar_blocks:
                 R.r.ctx.set_param("ar_blocks", args.ar_blocks)
             # each launch is timed as a complete collective (exit barrier on); in a training
@@ -77,7 +80,11 @@ def main():
             R.stream.synchronize()
             stream = R.stream
             ctx = R.r.ctx
-            fn = lambda t: ctx.allreduce_multicast(0, t, stream)   # noqa: E731
+            if args.multi_bucket:
+                nbk = R.n_buckets
+                fn = lambda t: ctx.allreduce_multicast(t % nbk, t // nbk, stream)   # noqa: E731
+            else:
+                fn = lambda t: ctx.allreduce_multicast(0, t, stream)   # noqa: E731
         times = []
         it = 0
         with torch.cuda.stream(stream):
@@ -97,7 +104,7 @@ def main():
         med = tt.item()
         if rank == 0:
             sec = med * 1e-3
-            print(json.dumps({"tag": args.tag, "mode": args.mode + ("_nvls" if args.nvls else ""), "burst": args.burst, "ar_blocks": args.ar_blocks, "oneshot_max": args.oneshot_max, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
+            print(json.dumps({"tag": args.tag, "multi_bucket": args.multi_bucket, "mode": args.mode + ("_nvls" if args.nvls else ""), "burst": args.burst, "ar_blocks": args.ar_blocks, "oneshot_max": args.oneshot_max, "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"),
                               "dtype": args.dtype, "n": n, "bytes": S, "ms": med,
                               "p10_ms": sorted(times)[len(times) // 10], "p90_ms": sorted(times)[9 * len(times) // 10],
                               "algbw_GBps": S / sec / 1e9, "busbw_GBps": 2 * (n - 1) / n * S / sec / 1e9,
