@@ -12,7 +12,10 @@ fit next to the filler in one GPU's HBM at n <= 4):
                  produces it, torch fused AdamW on the own shard, NCCL all_gather of the
                  updated parameters;
   ours_nockpt -- the library's reduce-scatter + sharded AdamW fused with the NVLink
-                 parameter all-gather (CM_FLAG_ZERO1 | CM_FLAG_NO_TAP);
+                 parameter all-gather (CM_FLAG_ZERO1 | CM_FLAG_NO_TAP); each bucket's sharded
+                 step runs right behind its reduce-scatter on the comm stream (cm_apply_bucket,
+                 SURVEY 8 f1), overlapping the rest of the backward (CM_BUCKET_STEP=0: one
+                 optimizer kernel after the last bucket, as round 1);
   ours_ckpt   -- the same with the per-iteration checkpoint: tap of every reduced shard,
                  shadow step on a low-priority side stream, host snapshot every K steps.
 The filler GEMMs are stock torch (the workload, not the path).
@@ -105,11 +108,15 @@ def run_arm(arm, args, rank, world, local):
         if getattr(args, "drain_ctas", -1) != -1:
             ctx.set_param("drain_ctas", args.drain_ctas)
 
+        bucket_step = os.environ.get("CM_BUCKET_STEP", "1") != "0"
+
         def reduce(b, t):
             ev = torch.cuda.Event()
             ev.record(stream)
             comm.wait_event(ev)
             ctx.allreduce_multicast(b, t, comm)
+            if bucket_step:
+                ctx.apply_bucket(b, t + 1, stream=comm, **W.HP)
 
         def optimize(t):
             stream.wait_stream(comm)
@@ -119,7 +126,7 @@ def run_arm(arm, args, rank, world, local):
         side = [R.side]
 
         def cleanup():
-            ok = ctx.verify(stream) == -1 if arm == "ours_ckpt" else None
+            ok = ctx.verify_ex(cm.CM_VERIFY_ALL, stream)[0] == cm.CM_OK if arm == "ours_ckpt" else None
             ctx.join(stream)
             stream.synchronize()
             ctx.finalize()

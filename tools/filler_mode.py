@@ -44,7 +44,7 @@ def main():
                                              "fp32 master + AdamW state, ZeRO-1; fwd/bwd replaced by bf16 GEMMs "
                                              "of 6*P*T FLOPs",
                "n_gpus": world, "tokens_per_gpu": args.tokens, "shadow": args.shadow,
-               "ring_depth": args.ring_depth, "persist_every": args.persist_every, "drain_ctas": args.drain_ctas,
+               "ring_depth": args.ring_depth, "persist_every": args.persist_every, "drain_ctas": args.drain_ctas, "env": {k: v for k, v in os.environ.items() if k.startswith("CM_")},
                "filler_only_ms": floor_ms, "filler_tflops": tflops, **out}
         if "nccl" in out and "ours_ckpt" in out:
             res["ckpt_overhead_pct_vs_nccl"] = (out["ours_ckpt"]["ms_per_iter"] / out["nccl"]["ms_per_iter"] - 1) * 100
