@@ -247,6 +247,8 @@ struct cm_ctx {
     std::vector<char> applied;
     int applied_count = 0;
     StepRec bucket_rec;                 // the step's scalars, fixed by its first bucket
+    int64_t grads_step = -1;            // the training step whose reduced gradients the grad
+                                        // buffer / staging hold (-1 after a restore)
     int64_t train_step = 0;
     int64_t shadow_enq = 0;
     int K = 1;                       // persist the host snapshot every K shadow steps
@@ -1951,6 +1953,7 @@ static cm_status apply_impl(cm_ctx* c, int64_t step, const StepRec& rec, void* s
     if (!c->no_tap && c->ce_tap)   // the caller may overwrite grads after this: taps first
         CU(cudaStreamWaitEvent(S(stream), c->ev_tap_done[slot], 0));
     c->train_step = step;
+    c->grads_step = step;
     c->opt_kind = rec.kind;
     return CM_OK;
 }
@@ -2237,6 +2240,9 @@ cm_status cm_verify_ex(cm_ctx* c, int32_t scope, int64_t* mismatch, int32_t* wha
         // vs what the training step consumed: shard r of the grad buffer (the caller has not
         // overwritten it since the step), or with ZeRO-1 the staging half it read
         const int slot = (int)((T - 1) % c->D);
+        if (c->grads_step != T)
+            return fail(c, CM_ERR_STATE, "CM_VERIFY_RING: no training step since the restore (the gradient "
+                                         "buffers hold nothing of step %lld)", (long long)T);
         if (!slot_complete(c->seg, c->hdr, c->D, (int)c->buckets.size(), T)) {
             *mismatch = -1;
             if (what) *what = 5;
@@ -2457,6 +2463,7 @@ cm_status cm_restore(cm_ctx* c, int64_t* restored, void* stream) {
     }
     c->last_s = s;
     c->last_kind = 0;
+    c->grads_step = -1;   // the gradient buffers hold nothing of step I
     c->cur_iter = I;
     std::fill(c->issued.begin(), c->issued.end(), 0);
     std::fill(c->applied.begin(), c->applied.end(), 0);
