@@ -73,7 +73,7 @@ def main():
                 R.r.ctx.set_param("ar_blocks", args.ar_blocks)
             # each launch is timed as a complete collective (exit barrier on); in a training
             # step the exits are lazy and the optimizer's entry barrier fences the iteration
-            R.r.ctx.set_param("lazy_exit", 0)
+            R.r.ctx.set_param("lazy_exit", int(os.environ.get("CM_LAZY_EXIT_SWEEP", "0")))
             if args.oneshot_max >= 0:
                 R.r.ctx.set_param("oneshot_max_bytes", args.oneshot_max)
             R.r.ctx.gen_grads(0, 0, 10, R.stream)
