@@ -294,6 +294,8 @@ struct ArParams {
     int64_t nf_step;               // the step that applies this reduce (iteration + 1)
     int pdl_wait;                  // 1: wait for the predecessor kernel (it may have written
                                    // this bucket's gradients) before the entry barrier
+    int pdl_mode;                  // experiments: bit 0 = no wait for the predecessor at exit,
+                                   // bit 1 = trigger the dependents after the data phase
 };
 
 // a reduced 16-byte vector (the value the tap and the all-gather store) is finite?  Else
@@ -394,7 +396,7 @@ template <typename G, int N>
 __global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P) {
     if (P.pdl_wait) pdl_wait_prior();
     if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 0);   // peers' grads are ready
-    pdl_launch_next();                                              // the next bucket may launch
+    if (!(P.pdl_mode & 2)) pdl_launch_next();                       // the next bucket may launch
 
     const int64_t stride = (int64_t)gridDim.x * kArThreads;
     int64_t q = blockIdx.x * (int64_t)kArThreads + threadIdx.x;
@@ -410,8 +412,9 @@ __global__ void __launch_bounds__(kArThreads) rs_tap_ag_kernel(const ArParams P)
         ar_load<G, N>(P, q, x);
         ar_reduce_store<G, N>(P, q, x);
     }
+    if (P.pdl_mode & 2) pdl_launch_next();
     ar_epilogue<N>(P);
-    pdl_wait_prior();   // complete after the predecessor (stream-order completion)
+    if (!(P.pdl_mode & 1)) pdl_wait_prior();   // complete after the predecessor (stream-order completion)
 }
 
 // Software-pipelined variant (cm_set_param("ar_impl", 1)): one block per SM, each thread

@@ -216,6 +216,7 @@ struct cm_ctx {
     int ar_blocks_user = 0;        // ar_blocks set explicitly: no size-dependent grid
     int64_t ar_grid_switch = 48ll << 20;   // buckets up to this many bytes: one block per SM
     bool pdl = false;              // programmatic dependent launch of the all-reduce kernels
+    int pdl_mode = 0;              // experiments (see ArParams::pdl_mode)
     bool persist_on_tap = false;   // snapshot persists on the tap-drain stream (one D2H queue)
     cudaStream_t last_s = nullptr; // stream of this context's latest launch on a caller stream,
     int last_kind = 0;             // and its kind (1: an all-reduce kernel, 0: anything else)
@@ -678,6 +679,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "ar_blocks" && value >= 1 && value <= kMaxBarrierBlocks) { c->ar_blocks_max = (int)value; c->ar_blocks_user = 1; }
     else if (k == "ar_grid_switch_bytes" && value >= 0) c->ar_grid_switch = value;
     else if (k == "pdl" && (value == 0 || value == 1)) c->pdl = value != 0;
+    else if (k == "pdl_mode" && value >= 0 && value <= 3) c->pdl_mode = (int)value;
     else if (k == "persist_queue" && (value == 0 || value == 1)) c->persist_on_tap = value != 0;
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
@@ -1542,6 +1544,7 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     // its all-reduce kernel of another bucket of the same iteration
     const bool pdl = c->pdl && c->barriers;
     P.pdl_wait = (pdl && c->last_s == s && c->last_kind == 1 && c->last_iter == t) ? 0 : 1;
+    P.pdl_mode = c->pdl_mode;
     P.nf = c->nfref();                          // non-finite reduced values -> CM_ERR_INVARIANT
     P.elem0 = B.off + (int64_t)c->rank * shard;
     P.nf_step = t + 1;
