@@ -46,6 +46,11 @@ __device__ __forceinline__ void mc_st_v4(void* p, const uint4& v) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
+// monotone announce: a barrier slot only ever grows, whatever order two launches' blocks of
+// the same index reach it in (atomic max with release semantics, system scope, over NVLink)
+__device__ __forceinline__ void max_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.sys.global.max.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -72,7 +77,10 @@ __device__ __forceinline__ void pdl_launch_next() { asm volatile("griddepcontrol
 // (region, block, src) in rank k's pad holds the last epoch src announced to k.
 // Epochs increase by one per collective launch and are identical on all ranks (every
 // rank issues the same sequence of collectives), so a flag can never be satisfied by a
-// stale value; ">=" tolerates a peer that already announced the next epoch.
+// stale value; ">=" tolerates a peer that already announced the next epoch.  Announcements
+// are an atomic max: with programmatic dependent launch two launches' blocks of one index
+// may announce out of order, and a plain store of the older epoch would move the slot
+// backwards and strand the peer (measured: a trap under PDL with exit barriers).
 struct Pads {
     uint32_t* p[kMaxRanks];
 };
@@ -84,7 +92,7 @@ __device__ __forceinline__ void block_barrier(const Pads& pads, int n, int rank,
     __syncthreads();   // all of this block's prior stores are ordered before the release
     if (threadIdx.x < (unsigned)n) {
         const int k = threadIdx.x;
-        st_release_sys(pad_slot(pads.p[k], region, blockIdx.x, rank), epoch);
+        max_release_sys(pad_slot(pads.p[k], region, blockIdx.x, rank), epoch);
         const uint32_t* mine = pad_slot(pads.p[rank], region, blockIdx.x, k);
         // A peer that never arrives (crashed rank, mismatched call sequence) must not hang
         // the GPU: after ~30 s of waiting the kernel traps and the error surfaces at the

@@ -217,6 +217,7 @@ struct cm_ctx {
     int64_t ar_grid_switch = 48ll << 20;   // buckets up to this many bytes: one block per SM
     bool pdl = false;              // programmatic dependent launch of the all-reduce kernels
     int pdl_mode = 0;              // experiments (see ArParams::pdl_mode)
+    bool pdl_force = false;        // test only: PDL even with exit barriers (deadlock regression)
     bool persist_on_tap = false;   // snapshot persists on the tap-drain stream (one D2H queue)
     cudaStream_t last_s = nullptr; // stream of this context's latest launch on a caller stream,
     int last_kind = 0;             // and its kind (1: an all-reduce kernel, 0: anything else)
@@ -678,7 +679,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "tma_blocks" && value >= 1 && value <= 65535) c->tma_blocks = (int)value;
     else if (k == "ar_blocks" && value >= 1 && value <= kMaxBarrierBlocks) { c->ar_blocks_max = (int)value; c->ar_blocks_user = 1; }
     else if (k == "ar_grid_switch_bytes" && value >= 0) c->ar_grid_switch = value;
-    else if (k == "pdl" && (value == 0 || value == 1)) c->pdl = value != 0;
+    else if (k == "pdl" && (value >= 0 && value <= 2)) { c->pdl = value != 0; c->pdl_force = value == 2; }
     else if (k == "pdl_mode" && value >= 0 && value <= 3) c->pdl_mode = (int)value;
     else if (k == "persist_queue" && (value == 0 || value == 1)) c->persist_on_tap = value != 0;
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
@@ -1541,8 +1542,11 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     P.ag = (c->n > 1 && !c->zero1) ? 1 : 0;   // ZeRO-1 gathers the updated params instead
     // PDL (multi-process ranks, cm_set_param "pdl"): wait for the predecessor only if it may
     // have touched this bucket, i.e. unless the previous launch of this context on `s` was
-    // its all-reduce kernel of another bucket of the same iteration
-    const bool pdl = c->pdl && c->barriers;
+    // its all-reduce kernel of another bucket of the same iteration.  Never with exit
+    // barriers: an exit barrier's ">=" could then be met by the NEXT launch's block of the
+    // same index (its entry barrier is ordered by the trigger, its exit is not).
+    const bool exit_barrier = !(c->lazy_exit || c->zero1);
+    const bool pdl = (c->pdl || c->pdl_force) && c->barriers && (!exit_barrier || c->pdl_force);
     P.pdl_wait = (pdl && c->last_s == s && c->last_kind == 1 && c->last_iter == t) ? 0 : 1;
     P.pdl_mode = c->pdl_mode;
     P.nf = c->nfref();                          // non-finite reduced values -> CM_ERR_INVARIANT
@@ -1550,7 +1554,7 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     P.nf_step = t + 1;
     // exit barrier only when the training step does not fence the iteration: ZeRO-1's
     // optimizer ends in a barrier; the replicated AdamW starts with one when lazy_exit
-    P.exit_barrier = (c->lazy_exit || c->zero1) ? 0 : 1;
+    P.exit_barrier = exit_barrier ? 1 : 0;
     // tap modes: fused (kernel stores to the host ring), staged (kernel stores to an HBM
     // staging half, a copy engine drains it to the ring), copy-engine (CE reads the reduced
     // shard back from the grad buffer after the kernel)
