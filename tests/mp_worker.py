@@ -132,6 +132,26 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = dist.get_world_size()
+    if mode == "kd_rule":
+        # R28: a host shadow across processes needs K >= 2 and D >= K + 1 (cm_connect)
+        numel = W.numels(W.c1())
+        try:
+            harness.DistRank(numel, cm.CM_F32, 1 << 20, name + "a", 2, cm.CM_SHADOW_HOST, 0, persist_every=1)
+            raise AssertionError("D=2, K=1 (-> 2) accepted")
+        except cm.CMError as e:
+            assert e.status == cm.CM_ERR_CONFIG, e
+        R = harness.DistRank(numel, cm.CM_F32, 1 << 20, name, 3, cm.CM_SHADOW_HOST, 0, persist_every=1)
+        assert R.r.ctx.info().persist_every == 2
+        R.step()
+        R.sync()
+        rk = dist.get_rank()
+        dist.barrier()
+        R.r.ctx.finalize()
+        for nm in (name, name + "a"):
+            cm.unlink_shadow(nm, rk)
+        dist.destroy_process_group()
+        print(f"rank {rk}: {mode} ok", flush=True)
+        return
     if mode == "model_parity":
         cd = model_parity(name)
         rk = dist.get_rank()

@@ -29,7 +29,7 @@ def counts():
                                   "parity_oneshot", "parity_oneshot_bf16", "parity_oneshot_direct",
                                   "parity_nvls", "parity_nvls_bf16", "parity_zero1_oneshot",
                                   "parity_bucket_step", "parity_bucket_step_zero1", "nonfinite",
-                                  "restore_soft", "model_parity"])
+                                  "restore_soft", "model_parity", "kd_rule"])
 def test_multiprocess(mode):
     for n in counts():
         name = f"cmmp{os.getpid()}_{mode}_{n}"
