@@ -219,6 +219,7 @@ struct cm_ctx {
     int pdl_mode = 0;              // experiments (see ArParams::pdl_mode)
     bool pdl_force = false;        // test only: PDL even with exit barriers (deadlock regression)
     bool persist_on_tap = false;   // snapshot persists on the tap-drain stream (one D2H queue)
+    bool n1_ce_stage = false;      // n == 1: a copy engine copies each bucket into staging
     cudaStream_t last_s = nullptr; // stream of this context's latest launch on a caller stream,
     int last_kind = 0;             // and its kind (1: an all-reduce kernel, 0: anything else)
     int64_t last_iter = -1;        // iteration of that all-reduce kernel
@@ -682,6 +683,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "pdl" && (value >= 0 && value <= 2)) { c->pdl = value != 0; c->pdl_force = value == 2; }
     else if (k == "pdl_mode" && value >= 0 && value <= 3) c->pdl_mode = (int)value;
     else if (k == "persist_queue" && (value == 0 || value == 1)) c->persist_on_tap = value != 0;
+    else if (k == "n1_copy_engine" && (value == 0 || value == 1)) c->n1_ce_stage = value != 0;
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
     else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
@@ -1639,6 +1641,12 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         else launch_os_t<BF16Tag>(c->n, og, s, O);
         c->launches++;
         CHECK_LAUNCH();
+    } else if (!skip_kernel && c->n == 1 && staged && !fused_tap && c->n1_ce_stage) {
+        // n == 1: the reduced value is the local gradient, so the "all-reduce" is only the copy
+        // of the bucket into the staging half; with "n1_copy_engine" a copy engine does it
+        // (no SM time; the optimizer kernels still check every value for non-finites)
+        TimedScope ts(c, 0, s);
+        CU(cudaMemcpyAsync(P.tap, c->peer_grad[0] + byte_off, (size_t)shard * c->es, cudaMemcpyDeviceToDevice, s));
     } else if (!skip_kernel) {
         TimedScope ts(c, 0, s);
         if (c->ar_impl == 1) {

@@ -316,3 +316,26 @@ def test_surviving_segment_is_never_replaced_implicitly():
         r2.ctx.finalize()
     finally:
         cm.unlink_shadow(name, 0)
+
+
+def test_n1_copy_engine_staging_bit_exact():
+    """n == 1 ablation "n1_copy_engine": the bucket's copy into the staging half by a copy
+    engine instead of a kernel; R, ring, p/m/v and shadow stay bitwise equal to the oracle."""
+    numel = W.numels(W.c1_ragged())
+    g = group(numel, 1, D=4, K=2)
+    for r in g.ranks:
+        r.ctx.set_param("n1_copy_engine", 1)
+    plan = O.Plan(numel, 1 << 20, 4, 1)
+    ref = O.Run(plan, seed=0, gscale=W.GRAD_SCALE, hp=HP_O)
+    try:
+        for t in range(5):
+            g.step()
+            ref.step()
+            g.sync()
+            r = g.ranks[0]
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p), err_msg=f"p t {t}")
+            np.testing.assert_array_equal(bits(t2np(r.v)), bits(ref.v), err_msg=f"v t {t}")
+            np.testing.assert_array_equal(bits(ring_flat(g, t % 4)), bits(ref.T), err_msg=f"tap t {t}")
+            all_ok(g)
+    finally:
+        close(g)
