@@ -106,3 +106,41 @@ def test_bucket_step_errors():
         assert e.value.status == cm.CM_ERR_STATE
     finally:
         _close(g)
+
+
+@pytest.mark.parametrize("zero1", [False, True])
+def test_restore_after_partial_bucket_steps(zero1):
+    """A kill in the middle of backward with per-bucket steps: some buckets of step 4 already
+    updated p (and, ZeRO-1, pushed it to every rank) when the trainer dies.  Restore must
+    return step 3 and the run continue bit-exact vs the oracle's uninterrupted run."""
+    n = 2
+    g = _group(n, cm.CM_F32, cm.CM_FLAG_ZERO1 if zero1 else 0)
+    plan = O.Plan(NUMEL, 1 << 20, 4, n)
+    hp_o = dict(lr=W.HP["lr"], b1=W.HP["beta1"], b2=W.HP["beta2"], eps=W.HP["eps"], wd=W.HP["weight_decay"])
+    ref = O.Run(plan, seed=0, gscale=W.GRAD_SCALE, hp=hp_o)
+    try:
+        for _ in range(3):
+            g.step()
+            ref.step()
+        g.gen()
+        for b in reversed(range(g.n_buckets)):
+            for r in g.ranks:
+                r.ctx.allreduce_multicast(b, 3, g.stream)
+        for b in range(g.n_buckets // 2 + 1):
+            for r in g.ranks:
+                r.ctx.apply_bucket(b, 4, stream=g.stream, **g.hp)
+        g.sync()
+        assert [r.ctx.restore(g.stream) for r in g.ranks] == [3, 3]
+        g.t = 3
+        for _ in range(3):
+            g.step()
+            ref.step()
+        g.sync()
+        for r in g.ranks:
+            np.testing.assert_array_equal(bits(t2np(r.p)), bits(ref.p))
+            if not zero1:
+                np.testing.assert_array_equal(bits(t2np(r.m)), bits(ref.m))
+                np.testing.assert_array_equal(bits(t2np(r.v)), bits(ref.v))
+            assert r.ctx.verify_ex(cm.CM_VERIFY_ALL, g.stream) == (cm.CM_OK, -1, None)
+    finally:
+        _close(g)
