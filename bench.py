@@ -687,6 +687,43 @@ def run_ours_nockpt(args, rank, world, local, numel, dtype, cap):
     return out
 
 
+def run_small_buckets(args, rank, world, local, nvls=False):
+    """SURVEY 8 row f2 on the multi-GPU line: 256 KiB buckets (64 tensors of 16,384 fp32 in
+    buckets of 4), below the one-shot threshold at n <= 8, so every bucket takes the one-shot
+    push kernel (NVLS: through the NVLink-SHARP multicast inbox); checkpointed steps with the
+    host shadow, then the checkpoint verified (shadow, host log, ring)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2507_13522_b200 import cm, harness
+    numel = [1 << 14] * 64
+    flags = cm.CM_FLAG_NVLS if nvls else 0
+    name = f"cmsmall_{os.environ.get('MASTER_PORT', '0')}_{int(nvls)}"
+    try:
+        R = harness.DistRank(numel, cm.CM_F32, 256 << 10, name, 9, cm.CM_SHADOW_HOST, flags, persist_every=8)
+    except cm.CMError as e:
+        return {"unavailable": str(e)[:200]}
+    c = R.r.ctx
+    for _ in range(args.warmup):
+        R.step()
+    R.sync()
+    dist.barrier()
+    c.timing(True)
+    ms = time_steps(R.step, [R.stream, R.side], args.steps, c)
+    kms, kcnt = c.timing(False)
+    ms = max_over_ranks(ms)
+    checks = {}
+    for nm, scope in (("shadow", cm.CM_VERIFY_SHADOW), ("host_log", cm.CM_VERIFY_HOST), ("ring", cm.CM_VERIFY_RING)):
+        checks[nm] = c.verify_ex(scope, R.stream)[0] == cm.CM_OK
+    ar_us = max_over_ranks(kms[0] / max(kcnt[0], 1)) * 1e3
+    out = {"ms_per_step": ms / args.steps, "buckets": R.n_buckets, "bucket_bytes": 256 << 10,
+           "allreduce_us_per_bucket": ar_us, "checkpoint_verified": checks,
+           "what": "one-shot push all-reduce (every bucket below the threshold)" + (" through NVLS multicast" if nvls else "")}
+    dist.barrier()
+    c.finalize()
+    cm.unlink_shadow(name, rank)
+    return out
+
+
 # ---------------------------------------------------------------------------- oracle arm
 def cpu_model():
     try:
@@ -793,6 +830,9 @@ def main():
         zres = run_ours(zargs, rank, world, local, name, numel, dtype, cap)
         variants["zero1"] = {"ms_per_step": zres["ms_step"], "value": zres["iters_per_s"] * world,
                              "shadow_bit_identical": zres["shadow_bit_identical"]}
+    if not args.no_variants and world > 1:
+        variants["small_buckets_oneshot"] = run_small_buckets(args, rank, world, local)
+        variants["small_buckets_nvls"] = run_small_buckets(args, rank, world, local, nvls=True)
     model = None
     if not args.no_model and args.workload == "gpt2":
         import types
