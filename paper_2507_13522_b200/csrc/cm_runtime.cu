@@ -220,6 +220,7 @@ struct cm_ctx {
     bool pdl_force = false;        // test only: PDL even with exit barriers (deadlock regression)
     bool persist_on_tap = false;   // snapshot persists on the tap-drain stream (one D2H queue)
     bool n1_ce_stage = false;      // n == 1: a copy engine copies each bucket into staging
+    bool shadow_after_train = false;  // the shadow step waits for the training step's optimizer
     cudaStream_t last_s = nullptr; // stream of this context's latest launch on a caller stream,
     int last_kind = 0;             // and its kind (1: an all-reduce kernel, 0: anything else)
     int64_t last_iter = -1;        // iteration of that all-reduce kernel
@@ -684,6 +685,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "pdl_mode" && value >= 0 && value <= 3) c->pdl_mode = (int)value;
     else if (k == "persist_queue" && (value == 0 || value == 1)) c->persist_on_tap = value != 0;
     else if (k == "n1_copy_engine" && (value == 0 || value == 1)) c->n1_ce_stage = value != 0;
+    else if (k == "shadow_after_train" && (value == 0 || value == 1)) c->shadow_after_train = value != 0;
     else if (k == "oneshot_max_bytes" && value >= 0 && value <= kOsSlotBytes) c->oneshot_max = value;
     else if (k == "drain_ctas" && value >= -1 && value <= 64) c->drain_ctas = (int)value;
     else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
@@ -2132,6 +2134,10 @@ cm_status cm_shadow_apply(cm_ctx* c, int64_t step, void* side_stream) {
     const int h = (int)(it & 1);
     const bool from_stage = c->staged_tap && c->stage_buf[h] && c->stage_iter[h] == it;
     if (from_stage) CU(cudaStreamWaitEvent(s, c->ev_ar_done[h], 0));
+    if (c->shadow_after_train) {   // ablation: start after the training step's optimizer kernel
+        const int k = (int)(step % cm_ctx::kStepEv);
+        if (c->ev_gstep[k] && c->ev_gstep_step[k] == step) CU(cudaStreamWaitEvent(s, c->ev_gstep[k], 0));
+    }
     else CU(cudaStreamWaitEvent(s, c->ev_tap_done[slot], 0));   // all taps of iteration step-1
     bool persisted = false;
     cm_status st = shadow_step_enqueue(c, step, c->slot_sc[slot], s, false, &persisted,
