@@ -220,7 +220,9 @@ struct cm_ctx {
     bool pdl_force = false;        // test only: PDL even with exit barriers (deadlock regression)
     bool persist_on_tap = false;   // snapshot persists on the tap-drain stream (one D2H queue)
     bool n1_ce_stage = false;      // n == 1: a copy engine copies each bucket into staging
-    bool shadow_after_train = false;  // the shadow step waits for the training step's optimizer
+    bool shadow_after_train = true;   // the shadow step waits for the training step's optimizer
+                                      // (measured: -0.2 ms per GPT-2 step at n=1, profiles/r02/
+                                      // r02u_model_n1_shadow_after_train_ab.jsonl)
     cudaStream_t last_s = nullptr; // stream of this context's latest launch on a caller stream,
     int last_kind = 0;             // and its kind (1: an all-reduce kernel, 0: anything else)
     int64_t last_iter = -1;        // iteration of that all-reduce kernel
