@@ -736,7 +736,7 @@ def cpu_model():
     return None
 
 
-def oracle_timing(numel, dtype, cap, n, budget_s, steps=1, warmup=0, omp=False):
+def oracle_timing(numel, dtype, cap, n, budget_s, steps=1, warmup=0, omp=False, fill_budget=False):
     """Time the CPU oracle (oracle/, as it stands) on a bounded random sample of the
     workload's elements: `warmup` untimed and `steps` timed iterations, each ONE iteration
     of the rank-order sum of n ranks' generated gradients + AdamW over the same k sampled
@@ -758,6 +758,9 @@ def oracle_timing(numel, dtype, cap, n, budget_s, steps=1, warmup=0, omp=False):
     cal.iterate()
     per = (time.perf_counter() - t0) / k0
     k = int(min(plan.total, max(k0, budget_s / per)))
+    if fill_budget and k == plan.total:
+        # the whole workload fits one iteration's budget: run more iterations instead
+        steps = int(min(200, max(steps, budget_s * steps / (per * k))))
     idx = np.sort(rng.choice(plan.total, k, replace=False)).astype(np.int64)
     run = O.SampleRun(W.SEED, n, dtype, W.GRAD_SCALE, idx, np.ones(k, np.uint8), omp=omp)
     for _ in range(warmup):
@@ -783,8 +786,8 @@ def oracle_timing(numel, dtype, cap, n, budget_s, steps=1, warmup=0, omp=False):
 def cpu_baseline(numel, dtype, cap, n, budget_s):
     """The oracle on the box's host cores: all cores (OpenMP build, the reported value) and
     one core, each ~budget_s/2 of work in 3 iterations."""
-    allc = oracle_timing(numel, dtype, cap, n, budget_s / 6, steps=3, warmup=0, omp=True)
-    one = oracle_timing(numel, dtype, cap, n, budget_s / 6, steps=3, warmup=0, omp=False)
+    allc = oracle_timing(numel, dtype, cap, n, budget_s / 6, steps=3, warmup=1, omp=True, fill_budget=True)
+    one = oracle_timing(numel, dtype, cap, n, budget_s / 6, steps=3, warmup=0, omp=False, fill_budget=True)
     allc["single_core"] = {k: one[k] for k in ("value", "cores", "ns_per_elem_iter", "full_iter_ms", "sample")}
     return allc
 
