@@ -41,9 +41,16 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, n = dist.get_rank(), dist.get_world_size()
-    numel = W.numels(W.gpt2_small())
+    llama = os.environ.get("CM_RESTORE_WORKLOAD", "gpt2") == "llama8b"
+    # GPT-2 (fp32, replicated AdamW, K=8, D=16) or the Llama-3-8B shape (bf16 grads, ZeRO-1:
+    # the replicated fp32 state of 8B parameters does not fit next to the shadow at n <= 4)
+    numel = W.numels(W.llama3_8b()) if llama else W.numels(W.gpt2_small())
+    dtype = cm.CM_BF16 if llama else cm.CM_F32
+    D, K = (9, 8) if llama else (16, 8)
     flags = cm.CM_FLAG_ATTACH if phase in ("phase2", "phase2kill") else 0
-    R = harness.DistRank(numel, cm.CM_F32, W.CAP_BYTES, name, 16, cm.CM_SHADOW_HOST, flags, persist_every=8)
+    if llama:
+        flags |= cm.CM_FLAG_ZERO1
+    R = harness.DistRank(numel, dtype, W.CAP_BYTES, name, D, cm.CM_SHADOW_HOST, flags, persist_every=K)
     if phase == "phase1":
         for _ in range(k):
             R.step()
@@ -61,6 +68,7 @@ def main():
         dist.barrier()
         os._exit(0)
     # phase 2: fresh processes, garbage training state
+    torch.cuda.synchronize()
     R.r.p.fill_(float("nan"))
     R.r.m.fill_(float("nan"))
     R.r.v.fill_(float("nan"))
@@ -85,24 +93,37 @@ def main():
     ok_shadow = R.r.ctx.verify_ex(cm.CM_VERIFY_ALL, R.stream)[0] == cm.CM_OK
     # sampled bitwise comparison with the oracle's uninterrupted trajectories
     from oracle import oracle as O
-    plan = O.Plan(numel, W.CAP_BYTES, 4, n)
+    plan = O.Plan(numel, W.CAP_BYTES, 2 if llama else 4, n)
     rng = np.random.default_rng(rank)
     idx = np.sort(rng.choice(plan.total, 1 << 14, replace=False)).astype(np.int64)
-    used = np.ones(len(idx), np.uint8)        # GPT-2 needs no padding at n <= 8
-    p, m, v, Rl = O.run_sample(W.SEED, n, O.F32, W.GRAD_SCALE, I + more, idx, used, lr=W.HP["lr"],
-                               b1=W.HP["beta1"], b2=W.HP["beta2"], eps=W.HP["eps"], wd=W.HP["weight_decay"])
+    bi = np.searchsorted(plan.bucket_off, idx, side="right") - 1
+    used = ((idx - plan.bucket_off[bi]) < plan.bucket_used[bi]).astype(np.uint8)
+    p, m, v, Rl = O.run_sample(W.SEED, n, O.BF16 if llama else O.F32, W.GRAD_SCALE, I + more, idx, used,
+                               lr=W.HP["lr"], b1=W.HP["beta1"], b2=W.HP["beta2"], eps=W.HP["eps"],
+                               wd=W.HP["weight_decay"])
     ti = torch.from_numpy(idx).to(R.r.p.device)
-    same = all(np.array_equal(a[ti].cpu().numpy().view(np.uint32), b.view(np.uint32))
-               for a, b in ((R.r.p, p), (R.r.m, m), (R.r.v, v)))
+    same = np.array_equal(R.r.p[ti].cpu().numpy().view(np.uint32), p.view(np.uint32))
+    if llama:     # m, v are shard-local: this rank's shard of the sampled elements
+        e = plan.bucket_padded[bi] // n
+        local = idx - plan.bucket_off[bi] - rank * e
+        mine = (local >= 0) & (local < e)
+        tj = torch.from_numpy((plan.bucket_off[bi] // n + local)[mine]).to(R.r.m.device)
+        same = same and np.array_equal(R.r.m[tj].cpu().numpy().view(np.uint32), m[mine].view(np.uint32)) \
+            and np.array_equal(R.r.v[tj].cpu().numpy().view(np.uint32), v[mine].view(np.uint32))
+    else:
+        same = same and all(np.array_equal(a[ti].cpu().numpy().view(np.uint32), b.view(np.uint32))
+                            for a, b in ((R.r.m, m), (R.r.v, v)))
     res = torch.tensor([restore_s, float(same and ok_shadow)], dtype=torch.float64, device=R.r.p.device)
     dist.all_reduce(res, op=dist.ReduceOp.MAX)
     ok_all = torch.tensor([float(same and ok_shadow)], dtype=torch.float64, device=R.r.p.device)
     dist.all_reduce(ok_all, op=dist.ReduceOp.MIN)
     if rank == 0:
-        print(json.dumps({"n": n, "killed_after_iterations": k, "kill_point": os.environ.get("CM_KILL_POINT", "step"),
+        print(json.dumps({"workload": "llama8b (ZeRO-1, bf16 grads)" if llama else "gpt2", "n": n,
+                          "restore_bytes_h2d_per_gpu": int(12 * plan.total / n),
+                          "killed_after_iterations": k, "kill_point": os.environ.get("CM_KILL_POINT", "step"),
                           "restored_step": I, "restore_s_max_over_ranks": res[0].item(),
                           "continued_iterations": more, "bit_exact_vs_oracle_and_shadow": bool(ok_all.item() == 1.0),
-                          "sampled_elements_per_rank": int(len(idx)), "persist_every": 8, "ring_depth": 16}),
+                          "sampled_elements_per_rank": int(len(idx)), "persist_every": K, "ring_depth": D}),
               flush=True)
     dist.barrier()
     R.r.ctx.finalize()
