@@ -60,6 +60,7 @@ def parse():
                          "in-kernel stores straight to the host ring; ce: copy engine reads the grad buffer back")
     ap.add_argument("--no-baseline", action="store_true", help="skip the NCCL + torch fused AdamW arm")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-mode", default="direct", choices=["direct", "landing"])
     ap.add_argument("--cpu-sample-s", type=float, default=12.0,
                     help="target seconds of oracle work for cpu_baseline (half all-core, half one core; 0 skips)")
     ap.add_argument("--zero1", action="store_true",
@@ -512,10 +513,11 @@ def run_e2e(args, R, S_bytes, es):
     """Per step: H2D copy of this step's gradients from pinned host memory, the hot path,
     and a D2H read of the step's result (the shadow's published step, 8 bytes).
 
-    The inputs are double-buffered like a data loader's prefetch: step t+1's gradients are
-    copied (copy stream) into an HBM landing buffer while step t runs, and moved into the
-    registered grad buffer (one HBM copy) when step t+1 starts.  Every timed step's H2D is
-    issued inside the timed region (the first one is not prefetched; the last step
+    mode "direct" (default): step t+1's gradients are copied (copy stream) straight into the
+    registered grad buffer as soon as step t's optimizer has read it, overlapping step t's
+    device->host drains.  mode "landing": copied into an HBM landing buffer while step t runs
+    and moved into the grad buffer (one HBM copy) when step t+1 starts.  Every timed step's
+    H2D is issued inside the timed region (the first one is not prefetched; the last step
     prefetches nothing), so the region holds exactly one input copy per step."""
     import torch
     from paper_2507_13522_b200 import cm
@@ -525,7 +527,8 @@ def run_e2e(args, R, S_bytes, es):
         R.r.ctx.gen_grads(R.seed, 10_000 + i, R.gscale, R.stream)
         R.stream.synchronize()
         host[i].copy_(grad)
-    land = torch.empty_like(grad)
+    direct = getattr(args, "e2e_mode", "direct") == "direct"
+    land = grad if direct else torch.empty_like(grad)
     cs = torch.cuda.Stream(grad.device)
     free = torch.cuda.Event()
     free.record(R.stream)
@@ -535,7 +538,7 @@ def run_e2e(args, R, S_bytes, es):
     st = {"i": 0, "k": 0, "ready": None}
 
     def h2d(t):
-        cs.wait_event(free)                                   # the landing buffer was consumed
+        cs.wait_event(free)                                   # the target buffer was consumed
         with torch.cuda.stream(cs):
             land.copy_(host[t & 1], non_blocking=True)
         ev = torch.cuda.Event()
@@ -546,15 +549,20 @@ def run_e2e(args, R, S_bytes, es):
         if st["ready"] is None:
             h2d(R.t)
         R.stream.wait_event(st["ready"])
-        with torch.cuda.stream(R.stream):
-            grad.copy_(land, non_blocking=True)
-        free.record(R.stream)
+        if not direct:
+            with torch.cuda.stream(R.stream):
+                grad.copy_(land, non_blocking=True)
+            free.record(R.stream)
         st["ready"] = None
-        if st["i"] + 1 < st["k"]:
+        if st["i"] + 1 < st["k"] and not direct:
             h2d(R.t + 1)                                      # prefetch: overlaps this step
         for b in range(R.n_buckets):
             c.allreduce_multicast(b, R.t, R.stream)
         c.apply_step(R.t + 1, stream=R.stream, **R.hp)
+        if direct:
+            free.record(R.stream)                             # the optimizer has read the grads
+            if st["i"] + 1 < st["k"]:
+                h2d(R.t + 1)                                  # overlaps this step's drains
         c.shadow_apply(R.t + 1, R.side)
         with torch.cuda.stream(R.stream):
             dev_flag.fill_(R.t + 1)
@@ -573,8 +581,11 @@ def run_e2e(args, R, S_bytes, es):
     ms = max_over_ranks(run(k))
     return {"value": 1000.0 / (ms / k) * R.n, "unit": UNIT, "h2d_bytes_per_step": S_bytes,
             "d2h_bytes_per_step": 8, "ms_per_step": ms / k,
-            "note": "pinned-host grads copied H2D each step inside the timed region (step t+1's "
-                    "copy overlaps step t, HBM landing buffer); per rank"}
+            "mode": "direct" if direct else "landing",
+            "note": "pinned-host grads copied H2D each step inside the timed region (" +
+                    ("straight into the registered grad buffer once step t's optimizer read it, "
+                     "overlapping step t's drains" if direct else "step t+1's copy overlaps step t, HBM "
+                     "landing buffer") + "); per rank"}
 
 
 def run_nccl_baseline(args, rank, world, local, numel, dtype, cap):
