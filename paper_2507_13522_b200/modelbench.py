@@ -22,6 +22,21 @@ def run_arm(arm, args, rank, world, local):
     from . import cm
     from .ddp import CheckmateDDP
     dev = torch.device("cuda", local)
+    # the step's tail after backward: an event on the compute stream when backward's kernels
+    # are done (for torch DDP: after its all-reduce wait at the end of backward) and one when
+    # the step is done (ours: after the library step on the compute stream, which waits for the
+    # communication stream's all-reduces and per-bucket optimizer steps)
+    marks = {"on": False, "pairs": [], "cur": None}
+
+    def mark(k):
+        if not marks["on"]:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream(dev))
+        if k == 0:
+            marks["cur"] = e
+        else:
+            marks["pairs"].append((marks["cur"], e))
     model = make_model(0).to(dev)
     model.train()
     g = torch.Generator(device=dev)
@@ -38,7 +53,9 @@ def run_arm(arm, args, rank, world, local):
             with torch.autocast("cuda", dtype=torch.bfloat16):
                 loss = ddp(tokens[i], labels=tokens[i]).loss
             loss.backward()
+            mark(0)
             opt.step()
+            mark(1)
         streams = []
         cleanup = lambda: None   # noqa: E731
     else:
@@ -97,7 +114,9 @@ def run_arm(arm, args, rank, world, local):
             with torch.autocast("cuda", dtype=torch.bfloat16):
                 loss = model(tokens[i], labels=tokens[i]).loss
             loss.backward()
+            mark(0)
             cd.step()
+            mark(1)
         streams = [cd.comm, cd.side] + ([load[2]] if load is not None else [])
 
         def cleanup():
@@ -115,6 +134,7 @@ def run_arm(arm, args, rank, world, local):
     a.record(cur)
     lags = []
     has_shadow = arm not in ("nccl",) and not (flags & (cm.CM_FLAG_NO_TAP | cm.CM_FLAG_NO_SHADOW))
+    marks["on"] = True
     for i in range(args.warmup, args.warmup + args.steps):
         it(i)
         if has_shadow:   # training steps issued minus the step the shadow has published
@@ -129,7 +149,9 @@ def run_arm(arm, args, rank, world, local):
     ok = cleanup()
     del model
     torch.cuda.empty_cache()
-    out = {"ms_per_iter": ms.item(), "shadow_bit_identical": ok, "drain_ctas": drain}
+    tail = sum(a.elapsed_time(b) for a, b in marks["pairs"]) / max(1, len(marks["pairs"]))
+    out = {"ms_per_iter": ms.item(), "shadow_bit_identical": ok, "drain_ctas": drain,
+           "tail_after_backward_ms": tail}
     if lags:
         out["shadow_lag_iters"] = {"max": max(lags), "mean": sum(lags) / len(lags),
                                    "what": "steps the host has issued minus the step the shadow published, "
