@@ -83,6 +83,12 @@ class CheckmateDDP:
         self.t = 0
         self.issued = 0
         self.bucket_step = bucket_step
+        # where the per-bucket steps run: right behind the all-reduce on the communication
+        # stream (default), or (CM_BUCKET_STREAM=low) on a lowest-priority stream of their own
+        # that waits for each bucket's all-reduce, so they yield SMs to the backward pass
+        self.opt = None
+        if bucket_step and os.environ.get("CM_BUCKET_STREAM", "comm") == "low":
+            self.opt = torch.cuda.Stream(self.dev, priority=0)
         self.probe = None
         for p in self.params:
             p.register_post_accumulate_grad_hook(self._hook)
@@ -98,7 +104,13 @@ class CheckmateDDP:
             self.comm.wait_event(ev)
             self.r.ctx.allreduce_multicast(b, self.t, self.comm)
             if self.bucket_step:
-                self.r.ctx.apply_bucket(b, self.t + 1, stream=self.comm, **self.hp)
+                s = self.comm
+                if self.opt is not None:
+                    e2 = torch.cuda.Event()
+                    e2.record(self.comm)
+                    self.opt.wait_event(e2)
+                    s = self.opt
+                self.r.ctx.apply_bucket(b, self.t + 1, stream=s, **self.hp)
             self.issued += 1
 
     def zero_grad(self):
@@ -113,6 +125,8 @@ class CheckmateDDP:
         assert self.issued == len(self.size), "backward did not produce every bucket"
         cur = torch.cuda.current_stream(self.dev)
         cur.wait_stream(self.comm)
+        if self.opt is not None:
+            cur.wait_stream(self.opt)
         self.r.ctx.apply_step(self.t + 1, stream=cur, **self.hp)   # (remaining buckets +) the step's record
         if self.probe is not None:
             self.probe.after_step(self)
