@@ -417,6 +417,9 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *   "lazy_exit"           1 (default): no exit barrier per bucket, the training step's
  *                         optimizer kernel starts with one iteration fence; 0: an exit
  *                         barrier per bucket (each all-reduce a complete collective)
+ *   "pdl_mode"            experiments on the PDL trigger (bit 0: no wait for the predecessor
+ *                         before exit -- completion order no longer guaranteed; bit 1: trigger
+ *                         after the data phase); default 0
  *   "pdl"                 1: launch the all-reduce kernels with programmatic dependent launch
  *                         (multi-process ranks): the next bucket's kernel launches and passes
  *                         its entry barrier while the previous one still moves data.  It waits
@@ -424,7 +427,9 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *                         context's all-reduces, so the caller must not write gradients with
  *                         its own kernels on the all-reduce stream between two calls (produce
  *                         them on another stream + event, as a DDP comm stream does).  0
- *                         (default): plain stream order
+ *                         (default): plain stream order.  Only with lazy exits (an all-reduce
+ *                         with an exit barrier is launched in plain stream order); 2 forces
+ *                         PDL with exit barriers too (test of the monotone barrier slots)
  *   "ar_grid_switch_bytes" buckets up to this size take one block per SM instead of the
  *                         co-resident cap (default 48 MiB; ignored once "ar_blocks" is set)
  *   "ar_impl"             0 (default) unrolled two-shot kernel, 1 software-pipelined variant
