@@ -1259,4 +1259,91 @@ __global__ void publish_range_kernel(volatile uint64_t* dst, int count, uint64_t
     __threadfence_system();
 }
 
+// ------------------------------------------------------------------ RS + tap + AG, bulk-copy pipeline
+// cm_set_param("ar_impl", 2): the same fused all-reduce with the data movement done by the
+// bulk-copy engine (TMA, 1-D cp.async.bulk).  One block per SM walks tiles of the shard; for
+// each tile one elected thread pulls the tile from all n ranks' buffers (n-1 of them over
+// NVLink) into a shared-memory stage (mbarrier complete_tx), all threads reduce the n copies
+// in rank order (reduce_vec: identical bits) into rank 0's slot, and the elected thread pushes
+// the result to the tap target and to all n ranks' buffers with bulk stores.  Two stages: the
+// next tile's pulls are in flight while this one is reduced and pushed.  Few threads, many
+// bytes in flight per SM, no per-thread address arithmetic on the NVLink stream.  Staged tap
+// or no tap only (a direct tap keeps the per-thread kernel).
+constexpr int kArTmaThreads = 256;
+constexpr int kArTmaStages = 2;
+template <int N> struct ArTma {
+    static constexpr int kTile = N <= 2 ? 16384 : (N <= 4 ? 12288 : 8192);   // bytes per rank per stage
+    static constexpr int kSmem = kArTmaStages * N * kTile;
+};
+
+template <typename G, int N>
+__global__ void __launch_bounds__(kArTmaThreads, 1) rs_tap_ag_tma_kernel(const ArParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[kArTmaStages];
+    constexpr int T = ArTma<N>::kTile;
+    constexpr int V = GT<G>::kPerVec;
+    if (P.pdl_wait) pdl_wait_prior();
+    if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 0);   // peers' grads are ready
+    pdl_launch_next();
+    const int64_t bytes = P.nvec * 16;
+    const int64_t ntiles = (bytes + T - 1) / T;
+    const bool leader = threadIdx.x == 0;
+    auto stage = [&](int st, int k) { return smem + ((size_t)st * N + k) * T; };
+    auto issue = [&](int64_t tile, int st) {
+        const int64_t off = tile * T;
+        const uint32_t len = (uint32_t)((bytes - off) < T ? (bytes - off) : T);
+        mbar_expect_tx(&bars[st], len * N);
+#pragma unroll
+        for (int k = 0; k < N; ++k) bulk_load(stage(st, k), P.buf[k] + off, len, &bars[st]);
+    };
+    if (leader) {
+        for (int st = 0; st < kArTmaStages; ++st) mbar_init(&bars[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (leader)
+        for (int st = 0; st < kArTmaStages; ++st) {
+            const int64_t tile = blockIdx.x + (int64_t)st * gridDim.x;
+            if (tile < ntiles) issue(tile, st);
+        }
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % kArTmaStages;
+        mbar_wait(&bars[st], (uint32_t)((it / kArTmaStages) & 1));
+        const int64_t off = tile * T;
+        const int len = (int)((bytes - off) < T ? (bytes - off) : T);
+        for (int q = threadIdx.x; q < len / 16; q += kArTmaThreads) {
+            uint4 x[N];
+#pragma unroll
+            for (int k = 0; k < N; ++k) x[k] = *reinterpret_cast<const uint4*>(stage(st, k) + q * 16);
+            const uint4 r = reduce_vec<G, N>(x);
+            nf_check_vec<G>(P.nf, P.nf_step, P.elem0 + (off / 16 + q) * V, r);
+            *reinterpret_cast<uint4*>(stage(st, 0) + q * 16) = r;   // the result replaces rank 0's copy
+        }
+        fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the bulk stores
+        __syncthreads();
+        if (leader) {
+            if (P.tap) bulk_store(P.tap + off, stage(st, 0), (uint32_t)len);
+            if (P.ag) {
+#pragma unroll
+                for (int k = 0; k < N; ++k) bulk_store(P.buf[k] + off, stage(st, 0), (uint32_t)len);
+            }
+            bulk_commit();
+            const int64_t next = tile + (int64_t)kArTmaStages * gridDim.x;
+            if (next < ntiles) {
+                bulk_wait_read0();   // the stores have read this stage; refill it
+                issue(next, st);
+            }
+        }
+    }
+    if (leader) {
+        bulk_wait0();                // every bulk store of this block has completed
+        fence_proxy_async_global();  // ... and is ordered before the generic releases below
+        __threadfence_system();
+    }
+    __syncthreads();
+    ar_epilogue<N>(P);
+    pdl_wait_prior();
+}
+
 }  // namespace cm

@@ -462,10 +462,12 @@ static void launch_ar_pipe_t(int n, dim3 grid, cudaStream_t s, const ArParams& P
 }
 
 // launch with programmatic stream serialization (PDL) when pdl is set (see cm_kernels.cuh)
-static cudaError_t launch_pdl(void (*k)(ArParams), dim3 grid, cudaStream_t s, bool pdl, const ArParams& P) {
+static cudaError_t launch_pdl(void (*k)(ArParams), dim3 grid, cudaStream_t s, bool pdl, const ArParams& P,
+                              int threads = kArThreads, size_t smem = 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(kArThreads);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -473,6 +475,36 @@ static cudaError_t launch_pdl(void (*k)(ArParams), dim3 grid, cudaStream_t s, bo
     cfg.attrs = pdl ? at : nullptr;
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k, P);
+}
+
+template <typename G, int N>
+static void set_ar_tma_smem() {
+    cudaFuncSetAttribute(rs_tap_ag_tma_kernel<G, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ArTma<N>::kSmem);
+}
+template <typename G>
+static void set_ar_tma_smem_all() {
+    set_ar_tma_smem<G, 2>(); set_ar_tma_smem<G, 3>(); set_ar_tma_smem<G, 4>(); set_ar_tma_smem<G, 5>();
+    set_ar_tma_smem<G, 6>(); set_ar_tma_smem<G, 7>(); set_ar_tma_smem<G, 8>();
+}
+template <typename G>
+static void launch_ar_tma_t(int n, dim3 grid, cudaStream_t s, const ArParams& P, bool pdl) {
+    switch (n) {
+        case 2: launch_pdl(rs_tap_ag_tma_kernel<G, 2>, grid, s, pdl, P, kArTmaThreads, ArTma<2>::kSmem); break;
+        case 3: launch_pdl(rs_tap_ag_tma_kernel<G, 3>, grid, s, pdl, P, kArTmaThreads, ArTma<3>::kSmem); break;
+        case 4: launch_pdl(rs_tap_ag_tma_kernel<G, 4>, grid, s, pdl, P, kArTmaThreads, ArTma<4>::kSmem); break;
+        case 5: launch_pdl(rs_tap_ag_tma_kernel<G, 5>, grid, s, pdl, P, kArTmaThreads, ArTma<5>::kSmem); break;
+        case 6: launch_pdl(rs_tap_ag_tma_kernel<G, 6>, grid, s, pdl, P, kArTmaThreads, ArTma<6>::kSmem); break;
+        case 7: launch_pdl(rs_tap_ag_tma_kernel<G, 7>, grid, s, pdl, P, kArTmaThreads, ArTma<7>::kSmem); break;
+        default: launch_pdl(rs_tap_ag_tma_kernel<G, 8>, grid, s, pdl, P, kArTmaThreads, ArTma<8>::kSmem); break;
+    }
+}
+static int64_t ar_tma_tile(int n) {
+    switch (n) {
+        case 2: return ArTma<2>::kTile;
+        case 3: return ArTma<3>::kTile;
+        case 4: return ArTma<4>::kTile;
+        default: return n <= 4 ? ArTma<4>::kTile : ArTma<8>::kTile;
+    }
 }
 
 template <typename G>
@@ -693,7 +725,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
     else if (k == "numa_node" && value >= -2 && value < 64 && !c->seg) c->numa_req = (int)value;
     else if (k == "drain_flush_bytes" && value >= 0 && value <= kDrainCoalesce) c->drain_flush = value;
-    else if (k == "ar_impl" && (value == 0 || value == 1)) c->ar_impl = (int)value;
+    else if (k == "ar_impl" && value >= 0 && value <= 2) c->ar_impl = (int)value;
     else if (k == "zero1_impl" && value >= 0 && value <= 2) c->zero1_impl = (int)value;
     else if (k == "ar_pipe_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_pipe_blocks = (int)value;
     // cost decomposition only (tools/model_mode.py): the staged tap's copy-engine drain is not
@@ -934,6 +966,9 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
     c->wt1_blocks = c->sms * std::max(wocc1, 1);
     CU(cudaFuncSetAttribute(adamw_tma_kernel<F32Tag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kTmaStages * TmaTile<F32Tag>::kStageBytes));
+    set_ar_tma_smem_all<F32Tag>();
+    set_ar_tma_smem_all<BF16Tag>();
+    CU(cudaGetLastError());
     CU(cudaFuncSetAttribute(adamw_tma_kernel<BF16Tag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kTmaStages * TmaTile<BF16Tag>::kStageBytes));
 
@@ -1653,7 +1688,13 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         CU(cudaMemcpyAsync(P.tap, c->peer_grad[0] + byte_off, (size_t)shard * c->es, cudaMemcpyDeviceToDevice, s));
     } else if (!skip_kernel) {
         TimedScope ts(c, 0, s);
-        if (c->ar_impl == 1) {
+        if (c->ar_impl == 2 && c->n > 1 && !fused_tap) {
+            // bulk-copy pipeline: one block per SM over tiles of the shard
+            const int64_t tiles = (P.nvec * 16 + ar_tma_tile(c->n) - 1) / ar_tma_tile(c->n);
+            const int tg = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->sms));
+            if (c->dtype == CM_F32) launch_ar_tma_t<F32Tag>(c->n, tg, s, P, pdl);
+            else launch_ar_tma_t<BF16Tag>(c->n, tg, s, P, pdl);
+        } else if (c->ar_impl == 1) {
             // one block per SM (co-resident by construction); the done counter of a direct
             // tap was advanced by `grid` above, re-base it on this grid
             const int pg = (int)std::max<int64_t>(1, std::min<int64_t>(

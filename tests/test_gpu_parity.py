@@ -639,14 +639,19 @@ def test_drain_modes_ring_and_restore_bit_exact(drain):
         close(g)
 
 
+@pytest.mark.parametrize("impl", [1, 2])
 @pytest.mark.parametrize("dtype", [cm.CM_F32, cm.CM_BF16])
-@pytest.mark.parametrize("n", [1, 2, 4, 8])
-def test_pipelined_allreduce_kernel_bit_exact(n, dtype):
-    """ar_impl=1 (software-pipelined two-shot kernel, one block per SM): same bits."""
-    numel = TABLES["mixed"]
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+def test_pipelined_allreduce_kernel_bit_exact(n, dtype, impl):
+    """ar_impl=1 (software-pipelined two-shot kernel, one block per SM) and ar_impl=2 (bulk-copy
+    pipeline: TMA pulls of every rank's tile into shared memory, bulk-store pushes of the
+    result; ragged last tiles): same bits."""
+    if impl == 2 and n == 1:
+        pytest.skip("ar_impl 2 is the multi-rank kernel (n = 1 has no reduction)")
+    numel = TABLES["mixed"] + [3 * 4096 + 8, 12288 * 3 // 4 + 16]
     g = make_group(numel, n, dtype)
     for r in g.ranks:
-        r.ctx.set_param("ar_impl", 1)
+        r.ctx.set_param("ar_impl", impl)
         r.ctx.set_param("ar_pipe_blocks", 7)      # several vectors per thread on these sizes
     plan, ref = oracle_for(numel, n, dtype, 1 << 20)
     try:
