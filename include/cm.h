@@ -432,7 +432,12 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *                         PDL with exit barriers too (test of the monotone barrier slots)
  *   "ar_grid_switch_bytes" buckets up to this size take one block per SM instead of the
  *                         co-resident cap (default 48 MiB; ignored once "ar_blocks" is set)
- *   "ar_impl"             0 (default) unrolled two-shot kernel, 1 software-pipelined variant
+ *   "ar_impl"             -1 (default) auto: the bulk-copy pipeline for buckets of at least
+ *                         "ar_tma_min_bytes" (default 12 MiB), the unrolled kernel below; 0
+ *                         unrolled two-shot kernel (per-thread 16-byte loads/stores), 1
+ *                         software-pipelined variant, 2 bulk-copy pipeline (TMA pulls of every
+ *                         rank's tile into shared memory, bulk-store pushes; staged tap / no
+ *                         tap, n >= 2) for every bucket
  *   "ar_pipe_blocks"      grid of ar_impl 1 (default 148, one block per SM)
  *   "zero1_impl"          ZeRO-1 AdamW + parameter all-gather kernel: 1 (default) two
  *                         4-element groups per thread in flight, 0 one (ablation), 2 the

@@ -209,7 +209,11 @@ struct cm_ctx {
     int ar_blocks_max = 296, adam_blocks = 1184, shadow_blocks = 296, misc_blocks = 1184;
     int ar_blocks_tap_only = 32;   // n == 1: the kernel is only the PCIe tap; leave SMs free
     int adamw_impl = 2;            // 0 vectorised, 1 TMA bulk-copy staged, 2 warp-tiled (measured best)
-    int ar_impl = 0;               // 0 unrolled two-shot, 1 software-pipelined (one block per SM)
+    int ar_impl = -1;              // -1 auto (bulk-copy pipeline from ar_tma_min bytes, else the
+                                   // unrolled kernel), 0 unrolled two-shot, 1 software-pipelined
+                                   // (one block per SM), 2 bulk-copy (TMA) pipeline always
+    int64_t ar_tma_min = 12ll << 20;   // auto: buckets of at least this many bytes take the bulk
+                                       // copies (measured: faster from 16 MiB, slower at 4-8 MiB)
     int zero1_impl = 1;            // ZeRO-1 AdamW + AG: 1 two groups per thread in flight, 0 one,
                                    // 2 tiles pushed by bulk copies (cp.async.bulk)
     int ar_pipe_blocks = 148;
@@ -725,7 +729,8 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "lazy_exit" && (value == 0 || value == 1)) c->lazy_exit = value;
     else if (k == "numa_node" && value >= -2 && value < 64 && !c->seg) c->numa_req = (int)value;
     else if (k == "drain_flush_bytes" && value >= 0 && value <= kDrainCoalesce) c->drain_flush = value;
-    else if (k == "ar_impl" && value >= 0 && value <= 2) c->ar_impl = (int)value;
+    else if (k == "ar_impl" && value >= -1 && value <= 2) c->ar_impl = (int)value;
+    else if (k == "ar_tma_min_bytes" && value >= 0) c->ar_tma_min = value;
     else if (k == "zero1_impl" && value >= 0 && value <= 2) c->zero1_impl = (int)value;
     else if (k == "ar_pipe_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_pipe_blocks = (int)value;
     // cost decomposition only (tools/model_mode.py): the staged tap's copy-engine drain is not
@@ -1688,7 +1693,9 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
         CU(cudaMemcpyAsync(P.tap, c->peer_grad[0] + byte_off, (size_t)shard * c->es, cudaMemcpyDeviceToDevice, s));
     } else if (!skip_kernel) {
         TimedScope ts(c, 0, s);
-        if (c->ar_impl == 2 && c->n > 1 && !fused_tap) {
+        const bool tma = c->n > 1 && !fused_tap &&
+                         (c->ar_impl == 2 || (c->ar_impl == -1 && B.padded * c->es >= c->ar_tma_min));
+        if (tma) {
             // bulk-copy pipeline: one block per SM over tiles of the shard
             const int64_t tiles = (P.nvec * 16 + ar_tma_tile(c->n) - 1) / ar_tma_tile(c->n);
             const int tg = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->sms));
