@@ -317,6 +317,9 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     drain_now = ctx.info().drain_ctas
     ms_max = max_over_ranks(ms)
     ms_step = ms_max / args.steps
+    by_rank = [None] * world
+    dist.all_gather_object(by_rank, round(ms / args.steps, 4))   # per-rank step times (skew)
+    ms_timed_pass = max_over_ranks(ms_timed_pass)
     iters_per_s = 1000.0 / ms_step
     # the checkpoint after the timed run, bitwise (cm_verify_ex synchronises): the shadow's
     # working state, the host log alone (snapshot + ring roll-forward = the restore source)
@@ -465,7 +468,8 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
               "checkpoint_verified": checks,
               "host_link_GBps": link, "S_bytes": S_bytes,
               "drain": "copy engine" if drain_now == 0 else f"SM drain, {drain_now} CTA(s)",
-              "host_issue_ms_per_step": host_issue, "ms_step_kernel_timing_pass": ms_timed_pass / args.steps}
+              "host_issue_ms_per_step": host_issue, "ms_step_kernel_timing_pass": ms_timed_pass / args.steps,
+              "ms_per_step_by_rank": by_rank}
 
     # ----- e2e: same metric through the public API with HOST gradient buffers
     if not args.no_e2e:
@@ -893,6 +897,7 @@ def main():
             "kernels": res["kernels"],
             "host_issue_ms_per_step": res["host_issue_ms_per_step"],
             "ms_step_kernel_timing_pass": res["ms_step_kernel_timing_pass"],
+            "ms_per_step_by_rank": res["ms_per_step_by_rank"],
             "host_link_GBps": res["host_link_GBps"],
         }
         print(json.dumps(line), flush=True)
