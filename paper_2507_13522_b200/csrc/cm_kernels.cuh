@@ -304,6 +304,7 @@ struct ArParams {
                                    // this bucket's gradients) before the entry barrier
     int pdl_mode;                  // experiments: bit 0 = no wait for the predecessor at exit,
                                    // bit 1 = trigger the dependents after the data phase
+    int tma_tile;                  // bulk-copy pipeline: bytes per rank per stage (multiple of 128)
 };
 
 // a reduced 16-byte vector (the value the tap and the all-gather store) is finite?  Else
@@ -1270,17 +1271,16 @@ __global__ void publish_range_kernel(volatile uint64_t* dst, int count, uint64_t
 // bytes in flight per SM, no per-thread address arithmetic on the NVLink stream.  Staged tap
 // or no tap only (a direct tap keeps the per-thread kernel).
 constexpr int kArTmaThreads = 256;
-constexpr int kArTmaStages = 2;
+constexpr int kArTmaMaxSmem = 200 * 1024;
 template <int N> struct ArTma {
-    static constexpr int kTile = N <= 2 ? 16384 : (N <= 4 ? 12288 : 8192);   // bytes per rank per stage
-    static constexpr int kSmem = kArTmaStages * N * kTile;
+    static constexpr int kTile = N <= 2 ? 16384 : (N <= 4 ? 12288 : 8192);   // default bytes per rank per stage
 };
 
-template <typename G, int N>
+template <typename G, int N, int kArTmaStages>
 __global__ void __launch_bounds__(kArTmaThreads, 1) rs_tap_ag_tma_kernel(const ArParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[kArTmaStages];
-    constexpr int T = ArTma<N>::kTile;
+    const int T = P.tma_tile;
     constexpr int V = GT<G>::kPerVec;
     if (P.pdl_wait) pdl_wait_prior();
     if (P.barriers) block_barrier(P.pads, N, P.rank, P.epoch, 0);   // peers' grads are ready

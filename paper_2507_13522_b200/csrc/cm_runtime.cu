@@ -214,6 +214,8 @@ struct cm_ctx {
                                    // (one block per SM), 2 bulk-copy (TMA) pipeline always
     int64_t ar_tma_min = 12ll << 20;   // auto: buckets of at least this many bytes take the bulk
                                        // copies (measured: faster from 16 MiB, slower at 4-8 MiB)
+    int ar_tma_tile_req = 0;           // bulk-copy tile bytes per rank per stage (0: by n)
+    int ar_tma_stages = 2;             // bulk-copy pipeline depth (2 or 3)
     int zero1_impl = 1;            // ZeRO-1 AdamW + AG: 1 two groups per thread in flight, 0 one,
                                    // 2 tiles pushed by bulk copies (cp.async.bulk)
     int ar_pipe_blocks = 148;
@@ -301,6 +303,13 @@ struct cm_ctx {
 };
 
 // ====================================================================== helpers
+static int ar_tma_tile(const cm_ctx* c) {
+    int t = c->ar_tma_tile_req;
+    if (t <= 0) t = c->n <= 2 ? ArTma<2>::kTile : (c->n <= 4 ? ArTma<4>::kTile : ArTma<8>::kTile);
+    const int cap = (kArTmaMaxSmem / (c->ar_tma_stages * c->n)) / 128 * 128;
+    return std::max(128, std::min(t, cap));
+}
+
 static cm_status fail(cm_ctx* c, cm_status s, const char* fmt, ...) {
     char buf[1024];
     va_list ap;
@@ -483,33 +492,34 @@ static cudaError_t launch_pdl(void (*k)(ArParams), dim3 grid, cudaStream_t s, bo
 
 template <typename G, int N>
 static void set_ar_tma_smem() {
-    cudaFuncSetAttribute(rs_tap_ag_tma_kernel<G, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ArTma<N>::kSmem);
+    cudaFuncSetAttribute(rs_tap_ag_tma_kernel<G, N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kArTmaMaxSmem);
+    cudaFuncSetAttribute(rs_tap_ag_tma_kernel<G, N, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kArTmaMaxSmem);
 }
 template <typename G>
 static void set_ar_tma_smem_all() {
     set_ar_tma_smem<G, 2>(); set_ar_tma_smem<G, 3>(); set_ar_tma_smem<G, 4>(); set_ar_tma_smem<G, 5>();
     set_ar_tma_smem<G, 6>(); set_ar_tma_smem<G, 7>(); set_ar_tma_smem<G, 8>();
 }
+template <typename G, int N>
+static void launch_ar_tma_n(dim3 grid, cudaStream_t s, const ArParams& P, bool pdl, int stages) {
+    const size_t smem = (size_t)stages * N * P.tma_tile;
+    if (stages == 3) launch_pdl(rs_tap_ag_tma_kernel<G, N, 3>, grid, s, pdl, P, kArTmaThreads, smem);
+    else launch_pdl(rs_tap_ag_tma_kernel<G, N, 2>, grid, s, pdl, P, kArTmaThreads, smem);
+}
 template <typename G>
-static void launch_ar_tma_t(int n, dim3 grid, cudaStream_t s, const ArParams& P, bool pdl) {
+static void launch_ar_tma_t(int n, dim3 grid, cudaStream_t s, const ArParams& P, bool pdl, int stages) {
     switch (n) {
-        case 2: launch_pdl(rs_tap_ag_tma_kernel<G, 2>, grid, s, pdl, P, kArTmaThreads, ArTma<2>::kSmem); break;
-        case 3: launch_pdl(rs_tap_ag_tma_kernel<G, 3>, grid, s, pdl, P, kArTmaThreads, ArTma<3>::kSmem); break;
-        case 4: launch_pdl(rs_tap_ag_tma_kernel<G, 4>, grid, s, pdl, P, kArTmaThreads, ArTma<4>::kSmem); break;
-        case 5: launch_pdl(rs_tap_ag_tma_kernel<G, 5>, grid, s, pdl, P, kArTmaThreads, ArTma<5>::kSmem); break;
-        case 6: launch_pdl(rs_tap_ag_tma_kernel<G, 6>, grid, s, pdl, P, kArTmaThreads, ArTma<6>::kSmem); break;
-        case 7: launch_pdl(rs_tap_ag_tma_kernel<G, 7>, grid, s, pdl, P, kArTmaThreads, ArTma<7>::kSmem); break;
-        default: launch_pdl(rs_tap_ag_tma_kernel<G, 8>, grid, s, pdl, P, kArTmaThreads, ArTma<8>::kSmem); break;
+        case 2: launch_ar_tma_n<G, 2>(grid, s, P, pdl, stages); break;
+        case 3: launch_ar_tma_n<G, 3>(grid, s, P, pdl, stages); break;
+        case 4: launch_ar_tma_n<G, 4>(grid, s, P, pdl, stages); break;
+        case 5: launch_ar_tma_n<G, 5>(grid, s, P, pdl, stages); break;
+        case 6: launch_ar_tma_n<G, 6>(grid, s, P, pdl, stages); break;
+        case 7: launch_ar_tma_n<G, 7>(grid, s, P, pdl, stages); break;
+        default: launch_ar_tma_n<G, 8>(grid, s, P, pdl, stages); break;
     }
 }
-static int64_t ar_tma_tile(int n) {
-    switch (n) {
-        case 2: return ArTma<2>::kTile;
-        case 3: return ArTma<3>::kTile;
-        case 4: return ArTma<4>::kTile;
-        default: return n <= 4 ? ArTma<4>::kTile : ArTma<8>::kTile;
-    }
-}
+// bytes per rank per stage: the configured tile, capped so stages x n x tile fits the smem cap
+static int ar_tma_tile(const cm_ctx* c);
 
 template <typename G>
 static void launch_ar_t(int n, dim3 grid, cudaStream_t s, const ArParams& P, bool pdl) {
@@ -731,6 +741,8 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "drain_flush_bytes" && value >= 0 && value <= kDrainCoalesce) c->drain_flush = value;
     else if (k == "ar_impl" && value >= -1 && value <= 2) c->ar_impl = (int)value;
     else if (k == "ar_tma_min_bytes" && value >= 0) c->ar_tma_min = value;
+    else if (k == "ar_tma_tile" && value >= 0 && value <= 65536 && value % 128 == 0) c->ar_tma_tile_req = (int)value;
+    else if (k == "ar_tma_stages" && (value == 2 || value == 3)) c->ar_tma_stages = (int)value;
     else if (k == "zero1_impl" && value >= 0 && value <= 2) c->zero1_impl = (int)value;
     else if (k == "ar_pipe_blocks" && value >= 1 && value <= kMaxBarrierBlocks) c->ar_pipe_blocks = (int)value;
     // cost decomposition only (tools/model_mode.py): the staged tap's copy-engine drain is not
@@ -1697,10 +1709,11 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
                          (c->ar_impl == 2 || (c->ar_impl == -1 && B.padded * c->es >= c->ar_tma_min));
         if (tma) {
             // bulk-copy pipeline: one block per SM over tiles of the shard
-            const int64_t tiles = (P.nvec * 16 + ar_tma_tile(c->n) - 1) / ar_tma_tile(c->n);
+            P.tma_tile = ar_tma_tile(c);
+            const int64_t tiles = (P.nvec * 16 + P.tma_tile - 1) / P.tma_tile;
             const int tg = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->sms));
-            if (c->dtype == CM_F32) launch_ar_tma_t<F32Tag>(c->n, tg, s, P, pdl);
-            else launch_ar_tma_t<BF16Tag>(c->n, tg, s, P, pdl);
+            if (c->dtype == CM_F32) launch_ar_tma_t<F32Tag>(c->n, tg, s, P, pdl, c->ar_tma_stages);
+            else launch_ar_tma_t<BF16Tag>(c->n, tg, s, P, pdl, c->ar_tma_stages);
         } else if (c->ar_impl == 1) {
             // one block per SM (co-resident by construction); the done counter of a direct
             // tap was advanced by `grid` above, re-base it on this grid

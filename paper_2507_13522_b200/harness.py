@@ -52,7 +52,8 @@ class Rank:
         self.ctx.set_param("pdl", 1)
         # A/B switches for tools (collective settings: every rank must use the same value)
         for key in ("lazy_exit", "drain_ctas", "oneshot_max_bytes", "ar_impl", "ar_pipe_blocks", "drain_flush_bytes",
-                    "numa_node", "zero1_impl", "shadow_blocks", "pdl", "ar_grid_switch_bytes", "ar_blocks", "persist_queue", "pdl_mode", "n1_copy_engine", "shadow_after_train", "ar_tma_min_bytes"):
+                    "numa_node", "zero1_impl", "shadow_blocks", "pdl", "ar_grid_switch_bytes", "ar_blocks", "persist_queue", "pdl_mode", "n1_copy_engine", "shadow_after_train", "ar_tma_min_bytes",
+                    "ar_tma_tile", "ar_tma_stages"):
             val = os.environ.get("CM_" + key.upper())
             if val is not None:
                 self.ctx.set_param(key, int(val))
