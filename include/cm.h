@@ -417,6 +417,9 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *   "lazy_exit"           1 (default): no exit barrier per bucket, the training step's
  *                         optimizer kernel starts with one iteration fence; 0: an exit
  *                         barrier per bucket (each all-reduce a complete collective)
+ *   "force_no_barriers"   profiling only, before cm_connect: in-process ranks on several GPUs run
+ *                         without the cross-GPU barriers, so ncu can serialise their kernels
+ *                         (the data is then not a valid all-reduce; the NVLink traffic is)
  *   "pdl_mode"            experiments on the PDL trigger (bit 0: no wait for the predecessor
  *                         before exit -- completion order no longer guaranteed; bit 1: trigger
  *                         after the data phase); default 0

@@ -224,6 +224,9 @@ struct cm_ctx {
     bool pdl = false;              // programmatic dependent launch of the all-reduce kernels
     int pdl_mode = 0;              // experiments (see ArParams::pdl_mode)
     bool pdl_force = false;        // test only: PDL even with exit barriers (deadlock regression)
+    bool force_no_barriers = false;   // profiling only: in-process ranks on several GPUs without
+                                      // the cross-GPU barriers (ncu serialises kernels; values
+                                      // are then meaningless, the NVLink traffic is real)
     bool persist_on_tap = false;   // snapshot persists on the tap-drain stream (one D2H queue)
     bool n1_ce_stage = false;      // n == 1: a copy engine copies each bucket into staging
     bool shadow_after_train = true;   // the shadow step waits for the training step's optimizer
@@ -731,6 +734,7 @@ cm_status cm_set_param(cm_ctx* c, const char* key, int64_t value) {
     else if (k == "ar_grid_switch_bytes" && value >= 0) c->ar_grid_switch = value;
     else if (k == "pdl" && (value >= 0 && value <= 2)) { c->pdl = value != 0; c->pdl_force = value == 2; }
     else if (k == "pdl_mode" && value >= 0 && value <= 3) c->pdl_mode = (int)value;
+    else if (k == "force_no_barriers" && (value == 0 || value == 1) && !c->connected) c->force_no_barriers = value != 0;
     else if (k == "persist_queue" && (value == 0 || value == 1)) c->persist_on_tap = value != 0;
     else if (k == "n1_copy_engine" && (value == 0 || value == 1)) c->n1_ce_stage = value != 0;
     else if (k == "shadow_after_train" && (value == 0 || value == 1)) c->shadow_after_train = value != 0;
@@ -1265,7 +1269,7 @@ cm_status cm_connect(cm_ctx* c, const void* blobs, size_t blob_len) {
     // ranks that share one device and one process are "virtual ranks": the caller issues
     // them on one stream in order, so no kernel ever waits for another and no barrier is
     // needed (B200_PROFILING.md: never spin across launches on one GPU).
-    c->barriers = !(all_local && same_dev);
+    c->barriers = !(all_local && same_dev) && !c->force_no_barriers;
     // Hard-kill safety of a host shadow shared by several processes: restore needs one step
     // that every shard can still reach.  When a rank's iteration-t kernel runs, every peer's
     // ring already holds step t-1 (its staging half of t-2 was drained), so a peer may be stuck
