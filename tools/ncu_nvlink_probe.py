@@ -38,16 +38,21 @@ for rk in ranks:
     torch.cuda.set_device(rk.device)
     rk.ctx.connect(blobs)
 streams = [torch.cuda.Stream(torch.device("cuda", rk.device)) for rk in ranks]
+# (the library enqueues on the calling thread's current device: set it per rank)
 for t in range(2):
     for rk, s in zip(ranks, streams):
+        torch.cuda.set_device(rk.device)
         rk.ctx.gen_grads(0, t, 10, s)
     for b in range(ranks[0].n_buckets):
         for rk, s in zip(ranks, streams):
+            torch.cuda.set_device(rk.device)
             rk.ctx.allreduce_multicast(b, t, s)
     for rk, s in zip(ranks, streams):
+        torch.cuda.set_device(rk.device)
         rk.ctx.apply_step(t + 1, stream=s, **W.HP)
     for s in streams:
         s.synchronize()
 print("probe ok", a.n, ranks[0].n_buckets)
 for rk in ranks:
+    torch.cuda.set_device(rk.device)
     rk.ctx.finalize()
