@@ -41,9 +41,10 @@ def main(path, n=2):
     print()
     for k in sorted({k for k, _ in tot}):
         t = tot[(k, "t")]
+        ratio = lambda a, b: f"{a / b:.3f}" if b > 0 else "n/a (no user bytes)"   # noqa: E731
         print(f"- `{k}`: user rx {tot[(k, 'rxu')] / 1e6:.1f} MB, tx {tot[(k, 'txu')] / 1e6:.1f} MB in {t * 1e6:.1f} µs "
-              f"summed over its launches (both GPUs); raw/user rx {tot[(k, 'rx')] / max(1, tot[(k, 'rxu')]):.3f}, "
-              f"tx {tot[(k, 'tx')] / max(1, tot[(k, 'txu')]):.3f}; user rate rx {tot[(k, 'rxu')] / t / 1e9:.0f} GB/s, "
+              f"summed over its launches (both GPUs); raw/user rx {ratio(tot[(k, 'rx')], tot[(k, 'rxu')])}, "
+              f"tx {ratio(tot[(k, 'tx')], tot[(k, 'txu')])}; user rate rx {tot[(k, 'rxu')] / t / 1e9:.0f} GB/s, "
               f"tx {tot[(k, 'txu')] / t / 1e9:.0f} GB/s")
 
 
