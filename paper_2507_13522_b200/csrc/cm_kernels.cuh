@@ -1275,8 +1275,9 @@ constexpr int kArTmaMaxSmem = 200 * 1024;
 template <int N> struct ArTma {
     // default bytes per rank per stage: small tiles keep every SM busy on the mid-size buckets
     // of a training step (measured in the step pattern: n=2 16 MiB 27.2 us with 4 KiB tiles vs
-    // 29.8 with 16 KiB; n=4 32 MiB 76.5 us with 8 KiB vs 78.7 with 12 KiB; equal from 64 MiB)
-    static constexpr int kTile = N <= 2 ? 4096 : 8192;
+    // 29.8 with 16 KiB; n=4 16 MiB 41.6 us with 4 KiB vs 42.8 with 8 KiB and 44.7 with 12 KiB,
+    // GPT-2 lockstep chain 67.3 vs 67.9 us; equal from 64 MiB)
+    static constexpr int kTile = 4096;
 };
 
 template <typename G, int N, int kArTmaStages>

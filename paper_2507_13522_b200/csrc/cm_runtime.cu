@@ -308,7 +308,7 @@ struct cm_ctx {
 // ====================================================================== helpers
 static int ar_tma_tile(const cm_ctx* c) {
     int t = c->ar_tma_tile_req;
-    if (t <= 0) t = c->n <= 2 ? ArTma<2>::kTile : (c->n <= 4 ? ArTma<4>::kTile : ArTma<8>::kTile);
+    if (t <= 0) t = ArTma<2>::kTile;
     const int cap = (kArTmaMaxSmem / (c->ar_tma_stages * c->n)) / 128 * 128;
     return std::max(128, std::min(t, cap));
 }
