@@ -231,6 +231,42 @@ cm_status cm_unlink_shadow(const char *shm_name, int32_t rank);
 cm_status cm_shadow_save(const char *shm_name, int32_t rank, const char *path);
 cm_status cm_shadow_load(const char *path, const char *shm_name, int32_t rank);
 uint32_t cm_crc32(const void *data, size_t n);
+
+/* Shadow serving (SPEC.md:422-430 serve_checkpoint, SPEC.md:411-421
+ * consolidate; sec 4.2.4 "each shadow node serves as a checkpoint to
+ * the training nodes simultaneously").  Host-only, no device or context: any process on
+ * the host may serve a live segment while training runs.  Only HOST-placed shadows hold
+ * host snapshot halves; a segment without them is CM_ERR_ARG.
+ * cm_shadow_query -- describe rank `rank`'s segment: layout, and the step held by each
+ *   snapshot half (-1 = invalid or being rewritten).  CM_ERR_ARG if the segment is missing
+ *   or malformed.
+ * cm_shadow_consolidate -- I = min over ranks 0..world_size-1 of the newest snapshot step
+ *   each shard holds (SPEC.md:413-416 min rule); every shard must still hold I in one of
+ *   its two halves (the retained previous half), else CM_ERR_STATE
+ *   ("consolidation failure").  All segments must agree on world size and layout hash
+ *   (CM_ERR_CONFIG).  *step_out = I.
+ * cm_shadow_serve -- copy elements [off, off+count) of the shard-local fp32 array `what`
+ *   (0 p, 1 m, 2 v; shard-local order: shard r of bucket b at element off_b/n, see
+ *   cm_plan_bucket_table) at step `step` from the snapshot half that holds it into the
+ *   caller's host buffer dst (count*4 bytes, any alignment), and return the IEEE CRC-32 of
+ *   the bytes served in *crc_out (may be NULL).  The half's step word is read before and
+ *   after the copy (the shadow sets it to -1 before rewriting a half): if it changed, the
+ *   bytes may be torn and the call returns CM_ERR_STATE (retry at a newer consolidated
+ *   step).  CM_ERR_ARG for a range outside the owned shard (off < 0, count < 0,
+ *   off+count > shard_numel), a bad `what`, or a missing segment; CM_ERR_STATE if no half
+ *   holds `step`.  count = 0 serves nothing (CRC of no bytes = 0).                     */
+typedef struct {
+    int32_t world_size, rank, dtype, ring_depth, n_buckets, pad0;
+    int64_t shard_numel;      /* elements of this rank's shard (sum of E_b / n)           */
+    uint64_t layout_hash;
+    int64_t shadow_step;      /* last step the shadow published                          */
+    int64_t half_step[2];     /* step held by each host snapshot half, -1 = invalid      */
+    int64_t nf_step;          /* first non-finite step reported, -1 = none               */
+} cm_shadow_desc;
+cm_status cm_shadow_query(const char *shm_name, int32_t rank, cm_shadow_desc *out);
+cm_status cm_shadow_consolidate(const char *shm_name, int32_t world_size, int64_t *step_out);
+cm_status cm_shadow_serve(const char *shm_name, int32_t rank, int64_t step, int32_t what, int64_t off,
+                          int64_t count, void *dst, uint32_t *crc_out);
 const char *cm_last_error(const cm_ctx *ctx);
 
 /* ------------------------------------------------------------------ hot path

@@ -33,7 +33,14 @@ EXPORTS = ["cm_plan_buckets", "cm_plan_bucket_table", "cm_init", "cm_register_bu
            "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step", "cm_apply_bucket", "cm_apply_bucket_sgd",
            "cm_apply_step_sgd", "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_verify_ex", "cm_check", "cm_barrier", "cm_get_info",
            "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_timing_bytes", "cm_set_param", "cm_join", "cm_shadow_save", "cm_shadow_load",
-           "cm_crc32"]
+           "cm_crc32", "cm_shadow_query", "cm_shadow_consolidate", "cm_shadow_serve"]
+
+
+class cm_shadow_desc(C.Structure):
+    _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("dtype", C.c_int32), ("ring_depth", C.c_int32),
+                ("n_buckets", C.c_int32), ("pad0", C.c_int32), ("shard_numel", C.c_int64),
+                ("layout_hash", C.c_uint64), ("shadow_step", C.c_int64), ("half_step", C.c_int64 * 2),
+                ("nf_step", C.c_int64)]
 
 
 class cm_config(C.Structure):
@@ -116,6 +123,10 @@ def lib():
         L.cm_shadow_save.argtypes = [C.c_char_p, C.c_int32, C.c_char_p]
         L.cm_shadow_load.argtypes = [C.c_char_p, C.c_char_p, C.c_int32]
         L.cm_crc32.argtypes = [C.c_void_p, C.c_size_t]
+        L.cm_shadow_query.argtypes = [C.c_char_p, C.c_int32, C.POINTER(cm_shadow_desc)]
+        L.cm_shadow_consolidate.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_int64)]
+        L.cm_shadow_serve.argtypes = [C.c_char_p, C.c_int32, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_void_p,
+                                      C.POINTER(C.c_uint32)]
         L.cm_timing.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.cm_timing_bytes.argtypes = [P, C.POINTER(C.c_int64)]
         for name in EXPORTS:
@@ -174,8 +185,44 @@ def shadow_load(path, name, rank):
         raise CMError(st, f"cm_shadow_load({path}, {name}, {rank})")
 
 
-def crc32(data: bytes) -> int:
-    return int(lib().cm_crc32(data, len(data)))
+def crc32(data) -> int:
+    """cm_crc32 of bytes, or of a contiguous numpy array's memory (no copy)."""
+    if isinstance(data, (bytes, bytearray)):
+        return int(lib().cm_crc32(bytes(data), len(data)))
+    assert data.flags.c_contiguous
+    return int(lib().cm_crc32(data.ctypes.data if data.nbytes else None, data.nbytes))
+
+
+def shadow_query(name, rank) -> "cm_shadow_desc":
+    """cm_shadow_query: layout and snapshot-half steps of a rank's host segment."""
+    d = cm_shadow_desc()
+    st = lib().cm_shadow_query(name.encode(), int(rank), C.byref(d))
+    if st != CM_OK:
+        raise CMError(st, f"cm_shadow_query({name}, {rank})")
+    return d
+
+
+def shadow_consolidate(name, world_size) -> int:
+    """cm_shadow_consolidate: the step I every shard can serve (min rule)."""
+    i = C.c_int64(-1)
+    st = lib().cm_shadow_consolidate(name.encode(), int(world_size), C.byref(i))
+    if st != CM_OK:
+        raise CMError(st, f"cm_shadow_consolidate({name}, {world_size})")
+    return i.value
+
+
+def shadow_serve(name, rank, step, what, off, count, out=None):
+    """cm_shadow_serve into a host float32 array (allocated if out is None) -> (array, crc32)."""
+    import numpy as np
+    if out is None:
+        out = np.empty(int(count), dtype=np.float32)
+    assert out.dtype == np.float32 and out.flags.c_contiguous and out.size >= count
+    crc = C.c_uint32(0)
+    st = lib().cm_shadow_serve(name.encode(), int(rank), int(step), int(what), int(off), int(count),
+                               out.ctypes.data if count else None, C.byref(crc))
+    if st != CM_OK:
+        raise CMError(st, f"cm_shadow_serve({name}, rank {rank}, step {step}, what {what}, [{off}, {off + count}))")
+    return out, crc.value
 
 
 def _stream_ptr(stream):

@@ -2820,6 +2820,105 @@ cm_status cm_shadow_load(const char* path, const char* shm_name, int32_t rank) {
     return rc;
 }
 
+// ---------------------------------------------------------------- shadow serving (f4)
+// SPEC.md:422-430 serve_checkpoint, SPEC.md:411-421 consolidate.  A
+// read-only mapping of a live (or loaded) host segment: any process on the host serves.
+namespace {
+struct SegView {
+    void* mp = MAP_FAILED;
+    size_t size = 0;
+    const SegHeader* h = nullptr;
+    SegView() = default;
+    SegView(const SegView&) = delete;
+    SegView& operator=(const SegView&) = delete;
+    ~SegView() { if (mp != MAP_FAILED) munmap(mp, size); }
+    // open rank `rank`'s segment read-only and check that it is one of ours with host halves
+    cm_status open(const char* shm_name, int32_t rank) {
+        if (!shm_name || rank < 0) return CM_ERR_ARG;
+        char name[256];
+        snprintf(name, sizeof name, "/%s.r%d", shm_name, rank);
+        int fd = shm_open(name, O_RDONLY, 0);
+        if (fd < 0) return CM_ERR_ARG;
+        struct stat st;
+        if (fstat(fd, &st) != 0 || (size_t)st.st_size < sizeof(SegHeader)) { close(fd); return CM_ERR_ARG; }
+        size = (size_t)st.st_size;
+        mp = mmap(nullptr, size, PROT_READ, MAP_SHARED, fd, 0);
+        close(fd);
+        if (mp == MAP_FAILED) return CM_ERR_ARG;
+        h = (const SegHeader*)mp;
+        if (h->magic != kMagic || h->version != kVersion || h->total != size || h->rank != rank ||
+            h->shadow_place != CM_SHADOW_HOST || h->shard_numel < 0 ||
+            h->state_off + 6 * (uint64_t)h->shard_numel * 4 > size)
+            return CM_ERR_ARG;
+        return CM_OK;
+    }
+    int64_t half(int i) const {
+        return __atomic_load_n((const int64_t*)&h->half_step[i], __ATOMIC_ACQUIRE);
+    }
+    int64_t newest() const { return std::max(half(0), half(1)); }
+    const float* array(int hf, int what) const {
+        return (const float*)((const char*)mp + h->state_off) + ((size_t)hf * 3 + what) * h->shard_numel;
+    }
+};
+}  // namespace
+
+cm_status cm_shadow_query(const char* shm_name, int32_t rank, cm_shadow_desc* out) {
+    if (!out) return CM_ERR_ARG;
+    SegView s;
+    cm_status st = s.open(shm_name, rank);
+    if (st != CM_OK) return st;
+    memset(out, 0, sizeof *out);
+    out->world_size = s.h->world_size;
+    out->rank = s.h->rank;
+    out->dtype = s.h->dtype;
+    out->ring_depth = s.h->ring_depth;
+    out->n_buckets = s.h->n_buckets;
+    out->shard_numel = s.h->shard_numel;
+    out->layout_hash = s.h->layout_hash;
+    out->shadow_step = s.h->shadow_step;
+    out->half_step[0] = s.half(0);
+    out->half_step[1] = s.half(1);
+    out->nf_step = s.h->nf_step;
+    return CM_OK;
+}
+
+cm_status cm_shadow_consolidate(const char* shm_name, int32_t world_size, int64_t* step_out) {
+    if (!shm_name || !step_out || world_size < 1 || world_size > kMaxRanks) return CM_ERR_ARG;
+    std::vector<SegView> v(world_size);
+    int64_t I = INT64_MAX;
+    for (int r = 0; r < world_size; ++r) {
+        cm_status st = v[r].open(shm_name, r);
+        if (st != CM_OK) return st;
+        if (v[r].h->world_size != world_size || v[r].h->layout_hash != v[0].h->layout_hash) return CM_ERR_CONFIG;
+        I = std::min(I, v[r].newest());
+    }
+    if (I < 0) return CM_ERR_STATE;                   // some shard holds no snapshot at all
+    for (int r = 0; r < world_size; ++r)
+        if (v[r].half(0) != I && v[r].half(1) != I) return CM_ERR_STATE;   // advanced past I twice
+    *step_out = I;
+    return CM_OK;
+}
+
+cm_status cm_shadow_serve(const char* shm_name, int32_t rank, int64_t step, int32_t what, int64_t off,
+                          int64_t count, void* dst, uint32_t* crc_out) {
+    if (what < 0 || what > 2 || off < 0 || count < 0 || (count > 0 && !dst)) return CM_ERR_ARG;
+    SegView s;
+    cm_status st = s.open(shm_name, rank);
+    if (st != CM_OK) return st;
+    if (off > s.h->shard_numel || count > s.h->shard_numel - off) return CM_ERR_ARG;   // outside the shard
+    if (step < 0) return CM_ERR_STATE;
+    const int hf = s.half(0) == step ? 0 : s.half(1) == step ? 1 : -1;
+    if (hf < 0) return CM_ERR_STATE;
+    memcpy(dst, s.array(hf, what) + off, (size_t)count * 4);
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    if (s.half(hf) != step) return CM_ERR_STATE;    // rewritten while we copied: torn
+    if (crc_out) {
+        crc_init();
+        *crc_out = crc32_update(0, (const unsigned char*)dst, (size_t)count * 4);
+    }
+    return CM_OK;
+}
+
 cm_status cm_unlink_shadow(const char* name, int32_t rank) {
     if (!name) return CM_ERR_ARG;
     char buf[256];

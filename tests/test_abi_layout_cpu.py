@@ -11,7 +11,7 @@ import pytest
 from paper_2507_13522_b200 import cm
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STRUCTS = [cm.cm_config, cm.cm_layer_table, cm.cm_adamw, cm.cm_sgd, cm.cm_info]
+STRUCTS = [cm.cm_config, cm.cm_layer_table, cm.cm_adamw, cm.cm_sgd, cm.cm_info, cm.cm_shadow_desc]
 
 
 def _c_layout(tmp_path):
