@@ -267,6 +267,24 @@ cm_status cm_shadow_query(const char *shm_name, int32_t rank, cm_shadow_desc *ou
 cm_status cm_shadow_consolidate(const char *shm_name, int32_t world_size, int64_t *step_out);
 cm_status cm_shadow_serve(const char *shm_name, int32_t rank, int64_t step, int32_t what, int64_t off,
                           int64_t count, void *dst, uint32_t *crc_out);
+
+/* cm_shadow_export -- write the checkpoint at `step` (step < 0: the consolidated step) of
+ * the n = world_size shards to `path` as a model file with per-tensor records (SPEC.md:
+ * 371-374 CheckpointFile: per-layer + optimizer records, checksum; SPEC.md:430 the
+ * reassembled model equals the consolidated checkpoint), in the tensor order of `table`
+ * (the table the run registered; its plan must match the segments' layout hash).
+ * Little-endian, no padding:
+ *   header (64 B): u64 magic "KCBTMODL", u32 version 1, i32 n_tensors, i32 world_size,
+ *     i32 grad dtype, i64 step, u64 layout hash, i64 cap_bytes, u32 CRC-32 of every byte
+ *     after the header, u32 pad[3];
+ *   per tensor i: i64 index, i64 numel, u32 CRC-32 of p, m, v, u32 pad; then p, m, v
+ *     (numel fp32 each, the tensor's elements in order; padding is not written).
+ * Written to `path`.tmp, fsync'd, renamed.  Host-only; may run while training runs (a half
+ * rewritten during the export is CM_ERR_STATE, nothing is left behind).  *step_out (may be
+ * NULL) = the step written.  CM_ERR_CONFIG if the table or world size does not match the
+ * segments; CM_ERR_STATE if a shard does not hold `step`; CM_ERR_ARG for I/O errors.    */
+cm_status cm_shadow_export(const char *shm_name, const cm_layer_table *table, int32_t world_size, int64_t step,
+                           const char *path, int64_t *step_out);
 const char *cm_last_error(const cm_ctx *ctx);
 
 /* ------------------------------------------------------------------ hot path

@@ -33,7 +33,8 @@ EXPORTS = ["cm_plan_buckets", "cm_plan_bucket_table", "cm_init", "cm_register_bu
            "cm_finalize", "cm_unlink_shadow", "cm_last_error", "cm_allreduce_multicast", "cm_apply_step", "cm_apply_bucket", "cm_apply_bucket_sgd",
            "cm_apply_step_sgd", "cm_shadow_apply", "cm_restore", "cm_gen_grads", "cm_init_state", "cm_verify", "cm_verify_ex", "cm_check", "cm_barrier", "cm_get_info",
            "cm_bucket_info", "cm_shadow_view", "cm_ring_view", "cm_timing", "cm_timing_bytes", "cm_set_param", "cm_join", "cm_shadow_save", "cm_shadow_load",
-           "cm_crc32", "cm_shadow_query", "cm_shadow_consolidate", "cm_shadow_serve"]
+           "cm_crc32", "cm_shadow_query", "cm_shadow_consolidate", "cm_shadow_serve",
+           "cm_shadow_export"]
 
 
 class cm_shadow_desc(C.Structure):
@@ -127,6 +128,8 @@ def lib():
         L.cm_shadow_consolidate.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_int64)]
         L.cm_shadow_serve.argtypes = [C.c_char_p, C.c_int32, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_void_p,
                                       C.POINTER(C.c_uint32)]
+        L.cm_shadow_export.argtypes = [C.c_char_p, C.POINTER(cm_layer_table), C.c_int32, C.c_int64, C.c_char_p,
+                                       C.POINTER(C.c_int64)]
         L.cm_timing.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.cm_timing_bytes.argtypes = [P, C.POINTER(C.c_int64)]
         for name in EXPORTS:
@@ -223,6 +226,18 @@ def shadow_serve(name, rank, step, what, off, count, out=None):
     if st != CM_OK:
         raise CMError(st, f"cm_shadow_serve({name}, rank {rank}, step {step}, what {what}, [{off}, {off + count}))")
     return out, crc.value
+
+
+def shadow_export(name, numel, grad_dtype, cap_bytes, world_size, path, step=-1) -> int:
+    """cm_shadow_export: the checkpoint at `step` (default consolidated) as a per-tensor
+    model file; returns the step written."""
+    t, keep = _layer_table(numel, grad_dtype, cap_bytes)
+    out = C.c_int64(-1)
+    st = lib().cm_shadow_export(name.encode(), C.byref(t), int(world_size), int(step), str(path).encode(),
+                                C.byref(out))
+    if st != CM_OK:
+        raise CMError(st, f"cm_shadow_export({name}, n={world_size}, step {step}, {path})")
+    return out.value
 
 
 def _stream_ptr(stream):

@@ -402,6 +402,16 @@ static bool plan(const int64_t* numel, int nt, int64_t cap, int es, int n, PlanO
     return true;
 }
 
+// The layout a segment was built for: tensor sizes, bucket cap, gradient dtype, n.
+static uint64_t layout_hash_of(const std::vector<int64_t>& numel, int64_t cap_bytes, int32_t dtype, int32_t n) {
+    uint64_t h = 0xCBF29CE484222325ull;
+    h = fnv1a(h, numel.data(), numel.size() * sizeof(int64_t));
+    h = fnv1a(h, &cap_bytes, sizeof cap_bytes);
+    h = fnv1a(h, &dtype, sizeof dtype);
+    h = fnv1a(h, &n, sizeof n);
+    return h;
+}
+
 // ---------------------------------------------------------------- AdamW scalars
 // Reading R5: fp64 arithmetic, one rounding to fp32 per scalar; R6: beta^s by s
 // repeated fp64 multiplications from 1.0 (cached incrementally: the same sequence).
@@ -947,12 +957,7 @@ cm_status cm_register_buckets(cm_ctx* c, const cm_layer_table* t, void* grad, fl
     c->shard_numel = po.total / c->n;
     c->numel.assign(t->numel, t->numel + t->n_tensors);
     c->cap_bytes = t->cap_bytes;
-    uint64_t h = 0xCBF29CE484222325ull;
-    h = fnv1a(h, c->numel.data(), c->numel.size() * sizeof(int64_t));
-    h = fnv1a(h, &c->cap_bytes, sizeof c->cap_bytes);
-    h = fnv1a(h, &c->dtype, sizeof c->dtype);
-    h = fnv1a(h, &c->n, sizeof c->n);
-    c->layout_hash = h;
+    c->layout_hash = layout_hash_of(c->numel, c->cap_bytes, c->dtype, c->n);
     c->grad = grad; c->p = p; c->m = m; c->v = v;
     CU(cudaSetDevice(c->dev));
     CU(cudaMalloc(&c->d_buckets, sizeof(BucketDev) * c->buckets.size()));
@@ -2916,6 +2921,113 @@ cm_status cm_shadow_serve(const char* shm_name, int32_t rank, int64_t step, int3
         crc_init();
         *crc_out = crc32_update(0, (const unsigned char*)dst, (size_t)count * 4);
     }
+    return CM_OK;
+}
+
+// Model checkpoint file (SPEC.md:371-374 CheckpointFile: per-layer records + checksum;
+// SPEC.md:430 "reassembled model equals consolidated checkpoint"): the consolidated step
+// gathered from the n shards into per-tensor records in the caller's tensor order.
+namespace {
+struct ModelFileHeader {
+    uint64_t magic;          // kModelMagic
+    uint32_t version;        // 1
+    int32_t n_tensors, world_size, dtype;
+    int64_t step;
+    uint64_t layout_hash;
+    int64_t cap_bytes;
+    uint32_t crc32;          // of every byte after this header
+    uint32_t pad[3];
+};
+static_assert(sizeof(ModelFileHeader) == 64, "model file header");
+struct TensorRecord {        // followed by p, m, v: numel fp32 each
+    int64_t index, numel;
+    uint32_t crc32[3];       // of p, m, v
+    uint32_t pad;
+};
+static_assert(sizeof(TensorRecord) == 32, "tensor record");
+constexpr uint64_t kModelMagic = 0x4C444F4D5442434Bull;   // bytes "KCBTMODL"
+}  // namespace
+
+cm_status cm_shadow_export(const char* shm_name, const cm_layer_table* t, int32_t world_size, int64_t step,
+                           const char* path, int64_t* step_out) {
+    if (!shm_name || !t || !t->numel || !path || world_size < 1 || world_size > kMaxRanks) return CM_ERR_ARG;
+    if (t->grad_dtype != CM_F32 && t->grad_dtype != CM_BF16) return CM_ERR_CONFIG;
+    PlanOut po;
+    if (!plan(t->numel, t->n_tensors, t->cap_bytes, t->grad_dtype == CM_F32 ? 4 : 2, world_size, po))
+        return CM_ERR_CONFIG;
+    const std::vector<int64_t> numel(t->numel, t->numel + t->n_tensors);
+    const uint64_t lh = layout_hash_of(numel, t->cap_bytes, t->grad_dtype, world_size);
+    if (step < 0) {
+        cm_status st = cm_shadow_consolidate(shm_name, world_size, &step);
+        if (st != CM_OK) return st;
+    }
+    std::vector<SegView> seg(world_size);
+    std::vector<int> hf(world_size);
+    for (int r = 0; r < world_size; ++r) {
+        cm_status st = seg[r].open(shm_name, r);
+        if (st != CM_OK) return st;
+        if (seg[r].h->world_size != world_size || seg[r].h->layout_hash != lh ||
+            seg[r].h->shard_numel != po.total / world_size)
+            return CM_ERR_CONFIG;
+        hf[r] = seg[r].half(0) == step ? 0 : seg[r].half(1) == step ? 1 : -1;
+        if (hf[r] < 0) return CM_ERR_STATE;
+    }
+    crc_init();
+    const std::string tmp = std::string(path) + ".tmp";
+    FILE* f = fopen(tmp.c_str(), "wb");
+    if (!f) return CM_ERR_ARG;
+    ModelFileHeader fh{};
+    fh.magic = kModelMagic;
+    fh.version = 1;
+    fh.n_tensors = t->n_tensors;
+    fh.world_size = world_size;
+    fh.dtype = t->grad_dtype;
+    fh.step = step;
+    fh.layout_hash = lh;
+    fh.cap_bytes = t->cap_bytes;
+    bool ok = fwrite(&fh, sizeof fh, 1, f) == 1;
+    uint32_t crc = 0;
+    std::vector<float> buf;
+    // bucket of each tensor (the planner's tensors of one bucket are contiguous in it)
+    std::vector<int> bucket_of(t->n_tensors, 0);
+    for (size_t b = 0; b < po.buckets.size(); ++b)
+        for (int i = 0; i < t->n_tensors; ++i)
+            if (po.tensor_off[i] >= po.buckets[b].off && po.tensor_off[i] < po.buckets[b].off + po.buckets[b].padded)
+                bucket_of[i] = (int)b;
+    for (int i = 0; ok && i < t->n_tensors; ++i) {
+        const BucketDev& B = po.buckets[bucket_of[i]];
+        const int64_t s = B.padded / world_size, lo = po.tensor_off[i], hi = lo + numel[i];
+        TensorRecord rec{};
+        rec.index = i;
+        rec.numel = numel[i];
+        buf.resize((size_t)numel[i] * 3);
+        for (int w = 0; w < 3; ++w) {
+            float* dst = buf.data() + (size_t)w * numel[i];
+            for (int r = 0; r < world_size; ++r) {   // the pieces of [lo, hi) rank r owns
+                const int64_t a = std::max(lo, B.off + r * s), e = std::min(hi, B.off + (r + 1) * s);
+                if (a < e)
+                    memcpy(dst + (a - lo), seg[r].array(hf[r], w) + B.shard_off + (a - B.off - r * s),
+                           (size_t)(e - a) * 4);
+            }
+            rec.crc32[w] = crc32_update(0, (const unsigned char*)dst, (size_t)numel[i] * 4);
+        }
+        crc = crc32_update(crc, (const unsigned char*)&rec, sizeof rec);
+        crc = crc32_update(crc, (const unsigned char*)buf.data(), buf.size() * 4);
+        ok = fwrite(&rec, sizeof rec, 1, f) == 1 && fwrite(buf.data(), 4, buf.size(), f) == buf.size();
+    }
+    // every half still holds `step`: nothing was rewritten under the copies (seqlock)
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    bool torn = false;
+    for (int r = 0; r < world_size; ++r) torn = torn || seg[r].half(hf[r]) != step;
+    fh.crc32 = crc;
+    ok = ok && fseek(f, 0, SEEK_SET) == 0 && fwrite(&fh, sizeof fh, 1, f) == 1;
+    ok = (fflush(f) == 0) && ok && (fsync(fileno(f)) == 0);
+    ok = (fclose(f) == 0) && ok;
+    if (!ok || torn || rename(tmp.c_str(), path) != 0) {
+        unlink(tmp.c_str());
+        return torn ? CM_ERR_STATE : CM_ERR_ARG;
+    }
+    if (step_out) *step_out = step;
     return CM_OK;
 }
 

@@ -107,3 +107,41 @@ def fetch_tensor(shm_name, smap: ShardMap, index, step=None, what="p", verify=Tr
     pieces = smap.pieces(lo, hi)
     _serve_into(shm_name, step, WHAT[what], pieces, dst, lo, verify, threads=4)
     return step, dst
+
+
+def export(shm_name, numel, grad_dtype, cap_bytes, world_size, path, step=None):
+    """Write the checkpoint at `step` (default: consolidated) as a per-tensor model file
+    (cm_shadow_export); returns the step written."""
+    return cm.shadow_export(shm_name, numel, grad_dtype, cap_bytes, world_size, path, -1 if step is None else step)
+
+
+MODEL_MAGIC = 0x4C444F4D5442434B     # "KCBTMODL"
+
+
+def read_model_file(path, verify=True):
+    """Parse a cm_shadow_export file (layout in include/cm.h) -> (header dict, [records]);
+    each record {"index", "p", "m", "v"}.  verify: the file CRC-32 and every array's."""
+    import struct
+    import zlib
+    raw = open(path, "rb").read()
+    magic, ver, nt, world, dtype, step, lh, cap, crc = struct.unpack_from("<QIiiiqQqI", raw, 0)
+    if magic != MODEL_MAGIC or ver != 1:
+        raise ValueError(f"{path}: not a model checkpoint file")
+    if verify and zlib.crc32(raw[64:]) != crc:
+        raise ValueError(f"{path}: CRC-32 mismatch")
+    hdr = {"n_tensors": nt, "world_size": world, "dtype": dtype, "step": step, "layout_hash": lh, "cap_bytes": cap}
+    recs, o = [], 64
+    for _ in range(nt):
+        idx, n, c0, c1, c2 = struct.unpack_from("<qqIII", raw, o)
+        o += 32
+        arrs = {}
+        for w, c in zip("pmv", (c0, c1, c2)):
+            a = np.frombuffer(raw, dtype=np.float32, count=n, offset=o)
+            if verify and zlib.crc32(a.tobytes()) != c:
+                raise ValueError(f"{path}: tensor {idx} {w}: CRC-32 mismatch")
+            arrs[w] = a
+            o += 4 * n
+        recs.append({"index": idx, **arrs})
+    if o != len(raw):
+        raise ValueError(f"{path}: {len(raw) - o} trailing bytes")
+    return hdr, recs

@@ -2,7 +2,8 @@
 SPEC.md:411-421 consolidate; sec 4.2.4): after a run with host snapshots
 every K steps, the consolidated checkpoint fetched from the n shards' host segments --
 every shard in parallel, CRC-32 checked -- equals the oracle's p, m, v at that step,
-bitwise, and so does the retained previous snapshot and every single tensor.  While
+bitwise, and so does the retained previous snapshot, every single tensor, and the
+per-tensor model file cm_shadow_export writes.  While
 training keeps running (the shadow rewriting halves under the reader), every fetch that
 succeeds equals the oracle at the step it names."""
 import os
@@ -45,7 +46,7 @@ def _close(g):
 
 @pytest.mark.parametrize("n,dtype,opt", [(1, cm.CM_F32, "adamw"), (2, cm.CM_F32, "adamw"), (4, cm.CM_BF16, "adamw"),
                                          (3, cm.CM_F32, "sgd")])
-def test_fetch_equals_oracle(n, dtype, opt):
+def test_fetch_equals_oracle(n, dtype, opt, tmp_path):
     K, D, T = 2, 3, 5
     g = _group(NUMEL, n, K, D, opt, dtype)
     es = 4 if dtype == cm.CM_F32 else 2
@@ -73,6 +74,15 @@ def test_fetch_equals_oracle(n, dtype, opt):
         with pytest.raises(cm.CMError) as e:                    # step 3 was never persisted
             serving.fetch(g._shm, smap, step=3)
         assert e.value.status == cm.CM_ERR_STATE
+        # the per-tensor model file of the consolidated step (cm_shadow_export)
+        path = tmp_path / "model.ckpt"
+        assert serving.export(g._shm, NUMEL, dtype, 1 << 20, n, path) == 4
+        hdr, recs = serving.read_model_file(path)
+        assert hdr["step"] == 4 and len(recs) == len(NUMEL)
+        for i, rec in enumerate(recs):
+            lo = smap.tensor_off[i]
+            for k, w in enumerate("pmv"):
+                np.testing.assert_array_equal(bits(rec[w]), bits(saved[4][k][lo:lo + NUMEL[i]]), err_msg=f"{w} {i}")
     finally:
         _close(g)
 

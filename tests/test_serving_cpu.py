@@ -38,9 +38,20 @@ def _shard(glob, buckets, n, r):
     return np.concatenate([glob[off + r * (E // n): off + (r + 1) * (E // n)] for off, E, _ in buckets])
 
 
-def _write_segment(name, n, r, halves, layout_hash=0xABCD, world=None):
+def _layout_hash(numel, cap, dtype, n):
+    """FNV-1a 64 over the int64 tensor sizes, the int64 cap, the int32 dtype and int32 n
+    (the segment header's layout hash, include/cm.h cm_register_buckets)."""
+    h = 0xCBF29CE484222325
+    for b in np.asarray(numel, np.int64).tobytes() + struct.pack("<qii", cap, dtype, n):
+        h = ((h ^ b) * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def _write_segment(name, n, r, halves, layout_hash=None, world=None):
     """halves: [(step, [p, m, v] shard arrays) or (-1, None)] x 2."""
     L = len(next(h[1][0] for h in halves if h[1] is not None))
+    if layout_hash is None:
+        layout_hash = _layout_hash(NUMEL, CAP, cm.CM_F32, world or n)
     state_off = 4096
     total = (state_off + 6 * L * 4 + 4095) // 4096 * 4096
     buf = bytearray(total)
@@ -151,6 +162,36 @@ def test_fetch_reassembles_the_model(segs, n):
         st, t = serving.fetch_tensor(name, smap, i, what="m")
         lo = smap.tensor_off[i]
         np.testing.assert_array_equal(t.view(np.uint32), _global(8, 1, smap.padded)[lo:lo + NUMEL[i]].view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_export_model_file(segs, tmp_path, n):
+    """the per-tensor model file of the consolidated step holds every
+    tensor's p, m, v exactly, each record and the file CRC-32-checked."""
+    name, smap = segs(n, [(12, 8)] * (n - 1) + [(8, 4)])
+    path = tmp_path / "model.ckpt"
+    assert serving.export(name, NUMEL, cm.CM_F32, CAP, n, path) == 8
+    hdr, recs = serving.read_model_file(path)
+    assert (hdr["step"], hdr["world_size"], hdr["n_tensors"]) == (8, n, len(NUMEL))
+    for i, rec in enumerate(recs):
+        lo = smap.tensor_off[i]
+        assert rec["index"] == i
+        for w, a in serving.WHAT.items():
+            np.testing.assert_array_equal(rec[w].view(np.uint32),
+                                          _global(8, a, smap.padded)[lo:lo + NUMEL[i]].view(np.uint32))
+    if n > 1:                                           # the retained half of the leading shards
+        with pytest.raises(cm.CMError) as e:
+            serving.export(name, NUMEL, cm.CM_F32, CAP, n, path, step=12)
+        assert e.value.status == cm.CM_ERR_STATE
+    with pytest.raises(cm.CMError) as e:                # another model's table
+        serving.export(name, NUMEL[:-1], cm.CM_F32, CAP, n, tmp_path / "x.ckpt")
+    assert e.value.status == cm.CM_ERR_CONFIG
+    assert not (tmp_path / "x.ckpt").exists() and not (tmp_path / "x.ckpt.tmp").exists()
+    raw = bytearray(path.read_bytes())
+    raw[64 + 32 + 5] ^= 1                               # one bit of tensor 0's p
+    path.write_bytes(bytes(raw))
+    with pytest.raises(ValueError):
+        serving.read_model_file(path)
 
 
 def _fetch_worker(name, n, q):
