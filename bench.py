@@ -333,7 +333,7 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
         if st != cm.CM_OK:
             checks[nm + "_mismatch"] = {"flat_index": mis, "what": what}
     mismatch = -1 if all(v for k, v in checks.items() if not k.endswith("_mismatch")) else 0
-    iso_ms, iso_cnt = isolated_kernels(args, dtype, cap, numel)
+    iso_ms, iso_cnt, iso_chain = isolated_kernels(args, dtype, cap, numel)
 
     # ----- per-kernel rooflines (average launch duration, live events on each kernel's stream)
     # and the step's binding resource.  Algorithmic bytes per unit are in DESIGN.md 6.
@@ -371,13 +371,20 @@ def run_ours(args, rank, world, local, name, numel, dtype, cap):
     ent["frac"] = ent["achieved"] / ent["peak"]
     kern["rs_tap_ag"] = ent
     if iso_cnt[0]:
-        iso_ar = max_over_ranks(iso_ms[0] / iso_cnt[0])
+        iso_ar = max_over_ranks(iso_chain)
+        iso_ev = max_over_ranks(iso_ms[0] / iso_cnt[0])
         b_ar = ent["bytes_per_launch"]
-        kern["rs_tap_ag_isolated"] = {"avg_ms": iso_ar, "launches": iso_cnt[0], "bound": ent["bound"],
+        kern["rs_tap_ag_isolated"] = {"avg_ms": iso_ar, "launches": 5 * nb, "bound": ent["bound"],
                                       "achieved": b_ar / (iso_ar * 1e-3) / 1e9, "peak": ent["peak"],
                                       "unit": ent["unit"], "bytes_per_launch": b_ar,
                                       "frac": b_ar / (iso_ar * 1e-3) / 1e9 / ent["peak"],
-                                      "what": "same kernel timed on its own: staged tap to HBM, no shadow, no device->host drain"}
+                                      "what": "same kernel on its own (staged tap to HBM, no shadow, no device->host "
+                                              "drain): each step's chain of launches between two events, divided by "
+                                              "the bucket count"}
+        kern["rs_tap_ag_isolated_per_kernel_events"] = {
+            "avg_ms": iso_ev, "launches": iso_cnt[0], "achieved": b_ar / (iso_ev * 1e-3) / 1e9,
+            "frac": b_ar / (iso_ev * 1e-3) / 1e9 / ent["peak"],
+            "what": "the same launches timed with an event pair around each kernel"}
     ad_ms = kms[1] / max(kcnt[1], 1)
     if args.zero1:
         # sharded AdamW on L = P/n elements, fused with the parameter all-gather: HBM es+24
@@ -494,7 +501,7 @@ def isolated_kernels(args, dtype, cap, numel):
     import torch.distributed as dist
     from paper_2507_13522_b200 import cm, harness
     if args.workload == "llama8b":
-        return [0.0] * 5, [0] * 5
+        return [0.0] * 5, [0] * 5, 0.0
     flags = cm.CM_FLAG_NO_SHADOW | (cm.CM_FLAG_ZERO1 if args.zero1 else 0)
     name = f"cmiso_{os.environ.get('MASTER_PORT', '0')}_{os.getpid()}"
     R = harness.DistRank(numel, dtype, cap, name, 2, cm.CM_SHADOW_HOST, flags)
@@ -508,9 +515,28 @@ def isolated_kernels(args, dtype, cap, numel):
         R.step(shadow=False)
     R.sync()
     ms, cnt = R.r.ctx.timing(False)
+    # the same launches as a chain: one event pair around each step's bucket loop (events
+    # between kernels, above, also keep the next kernel from launching early under PDL)
+    import torch
+    c = R.r.ctx
+    chain, reps = 0.0, 5
+    for _ in range(reps):
+        c.gen_grads(R.seed, R.t, R.gscale, R.stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(R.stream)
+        for b in range(R.n_buckets):
+            c.allreduce_multicast(b, R.t, R.stream)
+        e1.record(R.stream)
+        if R.opt == "sgd":
+            c.apply_step_sgd(R.t + 1, stream=R.stream, **R.hp)
+        else:
+            c.apply_step(R.t + 1, stream=R.stream, **R.hp)
+        R.t += 1
+        R.sync()
+        chain += e0.elapsed_time(e1)
     R.r.ctx.finalize()
     cm.unlink_shadow(name, dist.get_rank())
-    return ms, cnt
+    return ms, cnt, chain / (reps * R.n_buckets)
 
 
 def run_e2e(args, R, S_bytes, es):

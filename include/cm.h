@@ -478,8 +478,10 @@ cm_status cm_join(cm_ctx *ctx, void *stream);
  *                         before exit -- completion order no longer guaranteed; bit 1: trigger
  *                         after the data phase); default 0
  *   "pdl"                 1: launch the all-reduce kernels with programmatic dependent launch
- *                         (multi-process ranks): the next bucket's kernel launches and passes
- *                         its entry barrier while the previous one still moves data.  It waits
+ *                         (multi-process ranks, and n = 1): the next bucket's kernel launches
+ *                         and passes its entry barrier while the previous one still moves data
+ *                         (n = 1: the staging copies of consecutive buckets overlap their
+ *                         launch and ramp; 0.96 vs 0.69 of HBM per GPT-2 bucket).  It waits
  *                         for its stream predecessor only when that was not one of this
  *                         context's all-reduces, so the caller must not write gradients with
  *                         its own kernels on the all-reduce stream between two calls (produce

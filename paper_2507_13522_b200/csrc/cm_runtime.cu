@@ -1607,13 +1607,16 @@ cm_status cm_allreduce_multicast(cm_ctx* c, int32_t bucket, int64_t t, void* str
     P.rank = c->rank;
     P.barriers = c->barriers ? 1 : 0;
     P.ag = (c->n > 1 && !c->zero1) ? 1 : 0;   // ZeRO-1 gathers the updated params instead
-    // PDL (multi-process ranks, cm_set_param "pdl"): wait for the predecessor only if it may
+    // PDL (multi-process ranks or n == 1, cm_set_param "pdl"): wait for the predecessor only if it may
     // have touched this bucket, i.e. unless the previous launch of this context on `s` was
     // its all-reduce kernel of another bucket of the same iteration.  Never with exit
     // barriers: an exit barrier's ">=" could then be met by the NEXT launch's block of the
     // same index (its entry barrier is ordered by the trigger, its exit is not).
     const bool exit_barrier = !(c->lazy_exit || c->zero1);
-    const bool pdl = (c->pdl || c->pdl_force) && c->barriers && (!exit_barrier || c->pdl_force);
+    // n == 1 (no barriers): consecutive buckets' copies into staging overlap launch and ramp.
+    // Not for virtual ranks: rank k+1's kernel reads the bucket rank k's all-gather rewrites.
+    const bool pdl = (c->pdl || c->pdl_force) &&
+                     ((c->barriers && (!exit_barrier || c->pdl_force)) || c->n == 1);
     P.pdl_wait = (pdl && c->last_s == s && c->last_kind == 1 && c->last_iter == t) ? 0 : 1;
     P.pdl_mode = c->pdl_mode;
     P.nf = c->nfref();                          // non-finite reduced values -> CM_ERR_INVARIANT
