@@ -1,4 +1,4 @@
-"""Summary of ncu NVLink counters (tools/r02ao.sh; one process, 2 GPUs, barriers off) per
+"""Summary of ncu NVLink counters (tools/ncu_nvlink_probe.sh; one process, 2 GPUs, barriers off) per
 kernel launch of the last iteration: user bytes received / transmitted over NVLink against
 the algorithmic per-rank bytes of the launch ((n-1)/n of the bucket each way for the two-shot
 all-reduce: the pulls in, the all-gather pushes out; ZeRO-1: the pulls only, and the AdamW

@@ -1,4 +1,4 @@
-"""profiles/traffic.json from an ncu per-launch CSV (tools/r02_ncu.sh step 2): the measured
+"""profiles/traffic.json from an ncu per-launch CSV (tools/ncu_final.sh step 2): the measured
 DRAM bytes (read + write) per launch next to the algorithmic bytes of the SAME launches, for
 the kernels bench.py reports: the all-reduce (average over one iteration's 17 buckets; n=1,
 staged tap: a copy of the bucket into the HBM staging half, 2 S_b), the training AdamW
