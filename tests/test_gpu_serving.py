@@ -29,10 +29,10 @@ def _hp_o(opt):
     return dict(lr=W.HP["lr"], b1=W.HP["beta1"], b2=W.HP["beta2"], eps=W.HP["eps"], wd=W.HP["weight_decay"])
 
 
-def _group(numel, n, K, D, opt="adamw", dtype=cm.CM_F32, cap=1 << 20):
+def _group(numel, n, K, D, opt="adamw", dtype=cm.CM_F32, cap=1 << 20, flags=0):
     _ctr[0] += 1
     name = f"cmsv{os.getpid()}_{_ctr[0]}"
-    g = harness.VirtualGroup(numel, n, 0, dtype, cap, name, D, cm.CM_SHADOW_HOST, 0, persist_every=K, opt=opt)
+    g = harness.VirtualGroup(numel, n, 0, dtype, cap, name, D, cm.CM_SHADOW_HOST, flags, persist_every=K, opt=opt)
     g._shm = name
     return g
 
@@ -44,11 +44,14 @@ def _close(g):
         cm.unlink_shadow(g._shm, r)
 
 
-@pytest.mark.parametrize("n,dtype,opt", [(1, cm.CM_F32, "adamw"), (2, cm.CM_F32, "adamw"), (4, cm.CM_BF16, "adamw"),
-                                         (3, cm.CM_F32, "sgd")])
-def test_fetch_equals_oracle(n, dtype, opt, tmp_path):
+@pytest.mark.parametrize("n,dtype,opt,flags", [(1, cm.CM_F32, "adamw", 0), (2, cm.CM_F32, "adamw", 0),
+                                               (4, cm.CM_BF16, "adamw", 0), (3, cm.CM_F32, "sgd", 0),
+                                               (2, cm.CM_BF16, "adamw", cm.CM_FLAG_ZERO1)])
+def test_fetch_equals_oracle(n, dtype, opt, flags, tmp_path):
+    """flags = CM_FLAG_ZERO1: the trainers hold only their m/v shard, the shadow the same
+    shard-local layout; the served model is the same."""
     K, D, T = 2, 3, 5
-    g = _group(NUMEL, n, K, D, opt, dtype)
+    g = _group(NUMEL, n, K, D, opt, dtype, flags=flags)
     es = 4 if dtype == cm.CM_F32 else 2
     ref = O.Run(O.Plan(NUMEL, 1 << 20, es, n), seed=0, dtype=dtype, gscale=W.GRAD_SCALE, hp=_hp_o(opt), opt=opt)
     smap = serving.ShardMap(NUMEL, dtype, 1 << 20, n)

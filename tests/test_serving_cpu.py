@@ -135,6 +135,19 @@ def test_full_range_is_the_half_and_crc_is_zlib(segs):
     assert (d.world_size, d.rank, d.shard_numel, list(d.half_step)) == (2, 1, smap.shard_numel, [4, 6])
 
 
+def test_device_placed_shadow_is_not_served(segs):
+    """A DEVICE-placed shadow has no host snapshot halves: nothing to serve (CM_ERR_ARG)."""
+    name, smap = segs(1, [(2, 0)])
+    with open(f"/dev/shm/{name}.r0", "r+b") as f:
+        f.seek(32)
+        f.write(struct.pack("<i", cm.CM_SHADOW_DEVICE))   # SegHeader.shadow_place
+    for call in (lambda: cm.shadow_query(name, 0), lambda: cm.shadow_serve(name, 0, 2, 0, 0, 4),
+                 lambda: serving.consolidate(name, 1)):
+        with pytest.raises(cm.CMError) as e:
+            call()
+        assert e.value.status == cm.CM_ERR_ARG
+
+
 def test_requests_refused(segs):
     name, smap = segs(2, [(6, 4), (6, 4)])
     L = smap.shard_numel
