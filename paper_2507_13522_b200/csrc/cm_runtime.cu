@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -2699,17 +2700,17 @@ static_assert(sizeof(FileHeader) == 64, "file header");
 constexpr uint64_t kFileMagic = 0x454C49465442434Bull;   // bytes "KCBTFILE"
 
 uint32_t crc_tab[8][256];
-void crc_init() {
-    static bool done = false;
-    if (done) return;
-    for (uint32_t i = 0; i < 256; ++i) {
-        uint32_t c = i;
-        for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-        crc_tab[0][i] = c;
-    }
-    for (uint32_t i = 0; i < 256; ++i)
-        for (int t = 1; t < 8; ++t) crc_tab[t][i] = (crc_tab[t - 1][i] >> 8) ^ crc_tab[0][crc_tab[t - 1][i] & 0xFF];
-    done = true;
+void crc_init() {   // once per process; serving threads may call it concurrently
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+            crc_tab[0][i] = c;
+        }
+        for (uint32_t i = 0; i < 256; ++i)
+            for (int t = 1; t < 8; ++t) crc_tab[t][i] = (crc_tab[t - 1][i] >> 8) ^ crc_tab[0][crc_tab[t - 1][i] & 0xFF];
+    });
 }
 uint32_t crc32_update(uint32_t crc, const unsigned char* p, size_t n) {
     crc = ~crc;
