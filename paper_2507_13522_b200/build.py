@@ -7,8 +7,10 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = [os.path.join(HERE, "csrc", "cm_runtime.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "cm_kernels.cuh"), os.path.join(ROOT, "include", "cm.h")]
+SRC = [os.path.join(HERE, "csrc", "cm_runtime.cu"),     # device runtime + kernels
+       os.path.join(HERE, "csrc", "cm_persist.cc")]     # host-only persistence / serving
+DEPS = SRC + [os.path.join(HERE, "csrc", "cm_kernels.cuh"), os.path.join(HERE, "csrc", "cm_segment.h"),
+              os.path.join(ROOT, "include", "cm.h")]
 OUT = os.path.join(HERE, "libcm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
