@@ -71,7 +71,9 @@ def parse():
     ap.add_argument("--no-variants", action="store_true", help="skip the ZeRO-1 variant timing (N>1)")
     ap.add_argument("--no-model", action="store_true",
                     help="skip the GPT-2 model-mode arms (real fwd/bwd; checkpoint overhead vs NCCL DDP)")
-    ap.add_argument("--model-steps", type=int, default=10)
+    ap.add_argument("--model-steps", type=int, default=200,
+                    help="timed model-mode iterations per arm (SURVEY 8.d C2: 200, the paper's timing, PAPER.md:578)")
+    ap.add_argument("--model-warmup", type=int, default=20)
     ap.add_argument("--micro-batch", type=int, default=16)
     return ap.parse_args()
 
@@ -890,11 +892,12 @@ def main():
     if not args.no_model and args.workload == "gpt2":
         import types
         from paper_2507_13522_b200.modelbench import run_arm
-        margs = types.SimpleNamespace(steps=args.model_steps, warmup=max(3, args.warmup), micro_batch=args.micro_batch,
+        margs = types.SimpleNamespace(steps=args.model_steps, warmup=max(3, args.model_warmup), micro_batch=args.micro_batch,
                                       ring_depth=args.ring_depth, persist_every=args.persist_every, tap=args.tap,
                                       zero1=args.zero1)
         model = {arm: run_arm(arm, margs, rank, world, local) for arm in ("nccl", "ours_nockpt", "ours_ckpt")}
         model["ckpt_overhead_pct_vs_nccl"] = (model["ours_ckpt"]["ms_per_iter"] / model["nccl"]["ms_per_iter"] - 1) * 100
+        model["timed_iterations"], model["warmup_iterations"] = args.model_steps, margs.warmup
         model["config"] = (f"GPT-2 small, random init, random tokens, micro-batch {args.micro_batch} x seq 1024 per GPU, "
                            f"bf16 autocast fwd/bwd (stock PyTorch), DP{world}; ours: CheckmateDDP backward hooks, "
                            f"tap={args.tap}, persist_every={args.persist_every}")
