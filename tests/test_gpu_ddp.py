@@ -91,3 +91,46 @@ def test_grad_probe_model_parity_n1():
     finally:
         cd.finalize()
         cm.unlink_shadow(name, 0)
+
+
+def test_checkmate_ddp_checkpoint_served():
+    """Model mode end to end: after training steps with a snapshot every 2 steps, the
+    checkpoint fetched from the host segment (serving.fetch, another code path than the
+    trainer's buffers) equals the training state bitwise, and the exported per-tensor model
+    file holds every parameter tensor of the module."""
+    from paper_2507_13522_b200 import serving
+    from paper_2507_13522_b200.ddp import CheckmateDDP
+    dev = torch.device("cuda", 0)
+    model = tiny_gpt2().to(dev)
+    name = f"cmddps{os.getpid()}"
+    cd = CheckmateDDP(model, 0, 1, 0, cap_bytes=64 << 10, shm_name=name, ring_depth=4, persist_every=2)
+    r = cd.r
+    numel = [p.numel() for p in cd.params]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7)
+    try:
+        for _ in range(4):
+            tok = torch.randint(0, 1000, (4, 128), device=dev, generator=gen)
+            cd.zero_grad()
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                loss = model(tok, labels=tok).loss
+            loss.backward()
+            cd.step()
+        torch.cuda.synchronize()
+        cd.side.synchronize()
+        smap = serving.ShardMap(numel, cm.CM_F32, 64 << 10, 1)
+        step, got = serving.fetch(name, smap)
+        assert step == 4
+        for w, t in (("p", r.p), ("m", r.m), ("v", r.v)):
+            np.testing.assert_array_equal(got[w].view(np.uint32), t.cpu().numpy().view(np.uint32), err_msg=w)
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "model.ckpt")
+            assert serving.export(name, numel, cm.CM_F32, 64 << 10, 1, path) == 4
+            hdr, recs = serving.read_model_file(path)
+        for prm, rec in zip(cd.params, recs):
+            np.testing.assert_array_equal(rec["p"].view(np.uint32),
+                                          prm.detach().float().cpu().numpy().ravel().view(np.uint32))
+    finally:
+        cd.finalize()
+        cm.unlink_shadow(name, 0)
