@@ -279,3 +279,38 @@ def test_never_torn_while_rewritten():
         mm.close()
     finally:
         cm.unlink_shadow(name, 0)
+
+
+def test_shard_map_pieces_cover_each_element_once():
+    """Property check of the client's range mapping (R31): for random tables, world sizes and
+    flat ranges, the pieces tile [lo, hi) exactly once, each inside one rank's shard of one
+    bucket, at the shard-local offset the concatenation of that rank's bucket shards gives."""
+    from hypothesis import given, settings, strategies as st
+
+    @settings(max_examples=60, deadline=None)
+    @given(st.lists(st.integers(1, 5000), min_size=1, max_size=12), st.sampled_from([1, 2, 3, 4, 8]),
+           st.sampled_from([cm.CM_F32, cm.CM_BF16]), st.integers(1 << 10, 1 << 14), st.data())
+    def prop(numel, n, dtype, cap, data):
+        smap = serving.ShardMap(numel, dtype, cap, n)
+        lo = data.draw(st.integers(0, smap.padded - 1))
+        hi = data.draw(st.integers(lo + 1, smap.padded))
+        # reference: global index -> (rank, shard-local index) by concatenating bucket shards
+        owner = np.empty(smap.padded, np.int64)
+        local = np.empty(smap.padded, np.int64)
+        fill = [0] * n
+        for off, E, _ in smap.buckets:
+            s = E // n
+            for r in range(n):
+                owner[off + r * s: off + (r + 1) * s] = r
+                local[off + r * s: off + (r + 1) * s] = np.arange(fill[r], fill[r] + s)
+                fill[r] += s
+        assert fill == [smap.shard_numel] * n
+        seen = np.zeros(smap.padded, np.int64)
+        for r, loc, g, cnt in smap.pieces(lo, hi):
+            assert cnt > 0 and lo <= g and g + cnt <= hi
+            assert (owner[g:g + cnt] == r).all()
+            np.testing.assert_array_equal(local[g:g + cnt], np.arange(loc, loc + cnt))
+            seen[g:g + cnt] += 1
+        assert (seen[lo:hi] == 1).all() and seen[:lo].sum() == 0 and seen[hi:].sum() == 0
+
+    prop()
